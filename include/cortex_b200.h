@@ -1,0 +1,151 @@
+/*
+ * cortex_b200.h — C ABI of the B200 stage-engine kernels (libcortex_b200.so).
+ *
+ * The reference (arXiv 2510.14126 "Cortex", package `stagesim`) has no native
+ * code and no FFI: its engine is the pure-Python `EngineState`
+ * (/root/reference/pkg/src/stagesim/engines.py:101-246). These exports are the
+ * device-side half of that engine's state transitions; the Python host mirror
+ * (paper_2510_14126_b200/engine.py, `GpuEngineState`) keeps the reference's
+ * method names and calls these through ctypes. Each entry point below names the
+ * EngineState transition it implements.
+ *
+ * Conventions
+ *  - Every export returns int32: 0 = ok, <0 = error (CortexStatus). The host
+ *    raises InternalInvariantViolation (stagesim/errors.py:8) on non-zero.
+ *  - Pointers are device pointers unless stated; sizes are element counts.
+ *  - No allocation happens inside any call; the caller owns all buffers.
+ *  - Work is enqueued on `stream` (a cudaStream_t passed as void*); nothing
+ *    synchronises the host.
+ *  - Block tables are int32 matrices [rows, table_stride]; a sequence's row holds
+ *    its stage-prefix blocks (ceil(P/16)) followed by its private blocks.
+ *  - KV cache: one bf16 allocation cache[layer][k|v][block][kv_head][16][128];
+ *    k_row0 / v_row0 are the 128-wide row offsets of a layer's K and V planes.
+ */
+#ifndef CORTEX_B200_H_
+#define CORTEX_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(CORTEX_BUILDING)
+typedef struct CUstream_st* cortex_stream_t; /* == cudaStream_t */
+#else
+typedef void* cortex_stream_t; /* cudaStream_t */
+#endif
+
+enum {
+  CORTEX_OK = 0,
+  CORTEX_EBADARG = -1,
+  CORTEX_ECUDA = -2,
+  CORTEX_ENOBLOCKS = -3,
+  CORTEX_EUNSUPPORTED = -4
+};
+
+/* ABI version (major * 100 + minor). */
+int32_t cortex_abi_version(void);
+
+/* ---- KV block pool (bitmap, bit = 1 -> free) -------------------------------
+ * EngineState.admit (engines.py:142-166): cold prefix blocks + prompt blocks;
+ * the lazy per-16-token append during EngineState.advance_decode
+ * (engines.py:172-194).
+ * Requests are served in order, lowest free block first; request i writes its
+ * counts[i] block ids to table[rows[i]][cols[i] ...]. All-or-nothing: if the
+ * batch does not fit, nothing changes and *status is set to CORTEX_ENOBLOCKS.
+ */
+int32_t cortex_kv_alloc(uint32_t* bitmap, int32_t nblocks, int32_t id_base,
+                        const int32_t* counts, const int32_t* rows, const int32_t* cols,
+                        int32_t n_req, int32_t* table, int32_t table_stride, int32_t* status,
+                        cortex_stream_t stream);
+
+/* EngineState.complete_call (engines.py:206-214) frees the call's private
+ * blocks; EngineState.evict_idle_prefix (engines.py:219-226) frees a prefix.
+ * A double free or an id outside the pool sets *status = CORTEX_EBADARG. */
+int32_t cortex_kv_free(uint32_t* bitmap, int32_t nblocks, int32_t id_base, const int32_t* table,
+                       int32_t table_stride, const int32_t* rows, const int32_t* cols,
+                       const int32_t* counts, int32_t n_req, int32_t* status,
+                       cortex_stream_t stream);
+
+/* Warm admit (engines.py:149-150): copy a resident prefix's block ids into the
+ * call's row: table[dst_rows[i]][dst_cols[i] + k] = table[src_rows[i]][k]. */
+int32_t cortex_table_copy(int32_t* table, int32_t table_stride, const int32_t* src_rows,
+                          const int32_t* dst_rows, const int32_t* dst_cols,
+                          const int32_t* counts, int32_t n, cortex_stream_t stream);
+
+/* Free-block count (occupancy metric; adds into *out_free). */
+int32_t cortex_kv_count_free(const uint32_t* bitmap, int32_t nblocks, int32_t* out_free,
+                             cortex_stream_t stream);
+
+/* ---- TMA descriptors ---------------------------------------------------------
+ * Encode a 128-byte CUtensorMap (host memory at tmap_out) over a bf16 row-major
+ * matrix [rows, cols] with row pitch in bytes; box = (box_rows, box_cols),
+ * box_cols * 2 == 128 (SWIZZLE_128B). */
+int32_t cortex_tmap_encode_2d_bf16(void* tmap_out, const void* gptr, uint64_t rows, uint64_t cols,
+                                   uint64_t row_pitch_bytes, uint32_t box_rows,
+                                   uint32_t box_cols);
+
+/* ---- decoder forward (the GPU work behind admit's prefill and
+ * advance_decode's emitted tokens) -------------------------------------------- */
+
+/* tcgen05/TMEM GEMM: out[m, n] = sum_k X[m, k] W[n, k] (+ residual[m, n]).
+ * tmap_w over W [N, K] with box (128, 64); tmap_x over X [>= M, K] with box (32, 64).
+ * workspace / counters are used when cortex_gemm_splits(M, N, K) > 1. */
+int32_t cortex_gemm_splits(int32_t M, int32_t N, int32_t K);
+int32_t cortex_gemm_bf16(const void* tmap_w, const void* tmap_x, int32_t M, int32_t N, int32_t K,
+                         void* out, int32_t ldo, int32_t out_f32, const void* residual,
+                         int32_t ldr, float* workspace, uint64_t workspace_bytes,
+                         int32_t* counters, int32_t n_counters, cortex_stream_t stream);
+
+int32_t cortex_embed(const void* emb, const int32_t* tokens, const int32_t* index, int32_t n_tok,
+                     int32_t d, void* out, cortex_stream_t stream);
+
+int32_t cortex_rmsnorm(const void* x, const int32_t* rows, int32_t n_rows, const void* w,
+                       int32_t d, float eps, void* y, cortex_stream_t stream);
+
+/* RoPE on q/k + write k, v of each token into its paged slot
+ * (table[tok_row][tok_col], offset tok_off). */
+int32_t cortex_rope_kv_append(const void* qkv, void* q_out, void* cache, int64_t k_row0,
+                              int64_t v_row0, const int32_t* table, int32_t table_stride,
+                              const int32_t* tok_pos, const int32_t* tok_row,
+                              const int32_t* tok_col, const int32_t* tok_off,
+                              const float* cos_tab, const float* sin_tab, int32_t n_tok,
+                              int32_t hq, int32_t hkv, cortex_stream_t stream);
+
+int32_t cortex_swiglu(const void* gu, int32_t n_tok, int32_t f, void* act,
+                      cortex_stream_t stream);
+
+/* Greedy token per row; optional scatter into per-slot state. */
+int32_t cortex_argmax(const float* logits, int64_t ld, int32_t n_rows, int32_t vocab,
+                      int32_t* out_tok, const int32_t* slot, int32_t* slot_tok, int32_t* hist,
+                      int32_t hist_stride, const int32_t* hist_pos, cortex_stream_t stream);
+
+/* Paged decode attention (one query token per sequence), split along the
+ * context in fixed 256-token chunks + LSE combine. o_part/lse_part:
+ * [n_seqs, max_splits, Hq, 128] / [n_seqs, max_splits, Hq] fp32 workspace,
+ * max_splits >= max over seqs of cortex_decode_splits(prefix, kv_len). */
+int32_t cortex_decode_splits(int32_t prefix_len, int32_t kv_len);
+int32_t cortex_paged_decode_attn(const void* tmap_kv, const void* q, const int32_t* table,
+                                 int32_t table_stride, const int32_t* seq_row,
+                                 const int32_t* seq_prefix, const int32_t* seq_kvlen,
+                                 int32_t n_seqs, int32_t n_kv_heads, int32_t group,
+                                 int64_t k_row0, int64_t v_row0, float softmax_scale,
+                                 float* o_part, float* lse_part, int32_t max_splits, void* out,
+                                 cortex_stream_t stream);
+
+/* Paged prefill attention: the last seq_qlen[s] positions of each sequence
+ * attend causally to its prefix + private tokens. */
+int32_t cortex_paged_prefill_attn(const void* tmap_kv, const void* q, void* out,
+                                  const int32_t* table, int32_t table_stride,
+                                  const int32_t* seq_row, const int32_t* seq_prefix,
+                                  const int32_t* seq_kvlen, const int32_t* seq_qstart,
+                                  const int32_t* seq_qlen, int32_t n_seqs, int32_t max_qlen,
+                                  int32_t n_kv_heads, int32_t group, int64_t k_row0,
+                                  int64_t v_row0, float softmax_scale, cortex_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CORTEX_B200_H_ */

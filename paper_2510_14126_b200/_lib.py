@@ -1,0 +1,68 @@
+"""ctypes binding of libcortex_b200.so (the C ABI in include/cortex_b200.h).
+
+There is no fallback: if the library is missing or cannot be loaded the import
+of any op fails with an ImportError naming the build command.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from ctypes import c_float, c_int32, c_int64, c_uint64, c_void_p
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libcortex_b200.so"
+
+P = c_void_p
+I32 = c_int32
+I64 = c_int64
+U64 = c_uint64
+F32 = c_float
+
+# name -> argtypes (every export returns int32 status)
+SIGNATURES: dict[str, list] = {
+    "cortex_abi_version": [],
+    "cortex_kv_alloc": [P, I32, I32, P, P, P, I32, P, I32, P, P],
+    "cortex_kv_free": [P, I32, I32, P, I32, P, P, P, I32, P, P],
+    "cortex_table_copy": [P, I32, P, P, P, P, I32, P],
+    "cortex_kv_count_free": [P, I32, P, P],
+    "cortex_tmap_encode_2d_bf16": [P, P, U64, U64, U64, ctypes.c_uint32, ctypes.c_uint32],
+    "cortex_gemm_splits": [I32, I32, I32],
+    "cortex_gemm_bf16": [P, P, I32, I32, I32, P, I32, I32, P, I32, P, U64, P, I32, P],
+    "cortex_embed": [P, P, P, I32, I32, P, P],
+    "cortex_rmsnorm": [P, P, I32, P, I32, F32, P, P],
+    "cortex_rope_kv_append": [P, P, P, I64, I64, P, I32, P, P, P, P, P, P, I32, I32, I32, P],
+    "cortex_swiglu": [P, I32, I32, P, P],
+    "cortex_argmax": [P, I64, I32, I32, P, P, P, P, I32, P, P],
+    "cortex_decode_splits": [I32, I32],
+    "cortex_paged_decode_attn": [P, P, P, I32, P, P, P, I32, I32, I32, I64, I64, F32, P, P, I32,
+                                 P, P],
+    "cortex_paged_prefill_attn": [P, P, P, P, I32, P, P, P, P, P, I32, I32, I32, I32, I64, I64,
+                                  F32, P],
+}
+
+STATUS_NAMES = {0: "ok", -1: "bad argument", -2: "CUDA error", -3: "out of KV blocks",
+                -4: "unsupported"}
+
+_LIB: ctypes.CDLL | None = None
+
+
+def load() -> ctypes.CDLL:
+    """Load the library (once) and declare every export's signature."""
+    global _LIB
+    if _LIB is None:
+        if not LIB_PATH.exists():
+            raise ImportError(
+                f"{LIB_PATH} is missing; build it with `python -m paper_2510_14126_b200.build` "
+                "(there is no CPU fallback)"
+            )
+        lib = ctypes.CDLL(str(LIB_PATH))
+        for name, argtypes in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = argtypes
+            fn.restype = c_int32
+        _LIB = lib
+    return _LIB
+
+
+def exported_symbols() -> list[str]:
+    return list(SIGNATURES)

@@ -1,0 +1,306 @@
+// Row-wise and element-wise pieces of the decoder step: embedding gather,
+// RMSNorm (optionally gathering rows), RoPE + paged KV append, SwiGLU, and the
+// greedy argmax over the vocabulary. All are HBM-bound SIMT kernels with 16-byte
+// vector accesses; arithmetic is fp32, storage bf16.
+#include "common.cuh"
+
+namespace {
+
+constexpr int kHeadDim = 128;
+constexpr int kTile = 16;
+
+struct alignas(16) bf16x8 {
+  __nv_bfloat162 v[4];
+};
+
+CORTEX_DEVICE void unpack8(const bf16x8& x, float (&f)[8]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(x.v[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+CORTEX_DEVICE bf16x8 pack8(const float (&f)[8]) {
+  bf16x8 x;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) x.v[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return x;
+}
+
+// out[t] = emb[tok], tok = tokens[index ? index[t] : t]
+__global__ void embed_kernel(const __nv_bfloat16* __restrict__ emb, const int* __restrict__ tokens,
+                             const int* __restrict__ index, int d, __nv_bfloat16* __restrict__ out) {
+  const int t = blockIdx.x;
+  const int tok = tokens[index ? index[t] : t];
+  const bf16x8* src = reinterpret_cast<const bf16x8*>(emb + static_cast<int64_t>(tok) * d);
+  bf16x8* dst = reinterpret_cast<bf16x8*>(out + static_cast<int64_t>(t) * d);
+  for (int i = threadIdx.x; i < d / 8; i += blockDim.x) dst[i] = src[i];
+}
+
+CORTEX_DEVICE float block_sum(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int nw = blockDim.x / 32;
+  if (lane_id() == 0) red[warp_id()] = v;
+  __syncthreads();
+  float s = 0.f;
+  for (int i = 0; i < nw; ++i) s += red[i];
+  __syncthreads();
+  return s;
+}
+
+// y[r] = bf16(x[src] * rsqrt(mean(x[src]^2) + eps) * w), src = rows ? rows[r] : r
+__global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const int* __restrict__ rows,
+                               const __nv_bfloat16* __restrict__ w, int d, float eps,
+                               __nv_bfloat16* __restrict__ y) {
+  __shared__ float red[32];
+  const int r = blockIdx.x;
+  const int src = rows ? rows[r] : r;
+  const bf16x8* xr = reinterpret_cast<const bf16x8*>(x + static_cast<int64_t>(src) * d);
+  const bf16x8* wr = reinterpret_cast<const bf16x8*>(w);
+  bf16x8* yr = reinterpret_cast<bf16x8*>(y + static_cast<int64_t>(r) * d);
+  const int nvec = d / 8;
+  // d <= 8 * 4 * blockDim: keep up to 4 vectors per thread in registers
+  float f[4][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = threadIdx.x + k * blockDim.x;
+    if (i < nvec) {
+      unpack8(xr[i], f[k]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ss += f[k][e] * f[k][e];
+    }
+  }
+  const float tot = block_sum(ss, red);
+  const float rstd = rsqrtf(tot / static_cast<float>(d) + eps);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = threadIdx.x + k * blockDim.x;
+    if (i < nvec) {
+      float wf[8], o[8];
+      unpack8(wr[i], wf);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = f[k][e] * rstd * wf[e];
+      yr[i] = pack8(o);
+    }
+  }
+}
+
+// RoPE (rotate-half, pairs (i, i+64)) on q and k of each token, q -> q_out,
+// k and v -> paged cache row of (table[row][col], kv_head, off).
+struct RopeArgs {
+  const __nv_bfloat16* qkv;  // [T, (Hq + 2 Hkv) * 128]
+  __nv_bfloat16* q_out;      // [T, Hq, 128]
+  __nv_bfloat16* cache;      // base of the whole KV allocation (128-wide rows)
+  int64_t k_row0, v_row0;
+  const int* table;
+  int table_stride;
+  const int* tok_pos;  // [T] logical position (rope angle)
+  const int* tok_row;  // [T] block-table row
+  const int* tok_col;  // [T] block index within the row
+  const int* tok_off;  // [T] token offset inside the block
+  const float* cos_tab;  // [max_pos, 64]
+  const float* sin_tab;
+  int hq, hkv;
+};
+
+__global__ void rope_kv_append_kernel(const RopeArgs a) {
+  const int t = blockIdx.x;
+  const int pos = a.tok_pos[t];
+  const int ldq = (a.hq + 2 * a.hkv) * kHeadDim;
+  const __nv_bfloat16* src = a.qkv + static_cast<int64_t>(t) * ldq;
+  const float* ct = a.cos_tab + static_cast<int64_t>(pos) * 64;
+  const float* st = a.sin_tab + static_cast<int64_t>(pos) * 64;
+  const int block = a.table[static_cast<int64_t>(a.tok_row[t]) * a.table_stride + a.tok_col[t]];
+  const int off = a.tok_off[t];
+  // rotate q and k heads: (head, pair i) work items
+  const int n_rot = (a.hq + a.hkv) * 64;
+  for (int item = threadIdx.x; item < n_rot; item += blockDim.x) {
+    const int h = item / 64;
+    const int i = item % 64;
+    const __nv_bfloat16* xh = src + h * kHeadDim;
+    const float x0 = __bfloat162float(xh[i]);
+    const float x1 = __bfloat162float(xh[i + 64]);
+    const float c = ct[i], s = st[i];
+    const float y0 = x0 * c - x1 * s;
+    const float y1 = x1 * c + x0 * s;
+    __nv_bfloat16* dst;
+    if (h < a.hq) {
+      dst = a.q_out + (static_cast<int64_t>(t) * a.hq + h) * kHeadDim;
+    } else {
+      const int kh = h - a.hq;
+      dst = a.cache + (a.k_row0 + (static_cast<int64_t>(block) * a.hkv + kh) * kTile + off) * kHeadDim;
+    }
+    dst[i] = __float2bfloat16_rn(y0);
+    dst[i + 64] = __float2bfloat16_rn(y1);
+  }
+  // v: straight copy, 8 elements per item
+  const int n_v = a.hkv * kHeadDim / 8;
+  for (int item = threadIdx.x; item < n_v; item += blockDim.x) {
+    const int kh = item / (kHeadDim / 8);
+    const int e = item % (kHeadDim / 8);
+    const bf16x8* vs =
+        reinterpret_cast<const bf16x8*>(src + (a.hq + a.hkv + kh) * kHeadDim) + e;
+    bf16x8* vd = reinterpret_cast<bf16x8*>(
+                     a.cache + (a.v_row0 + (static_cast<int64_t>(block) * a.hkv + kh) * kTile + off) *
+                                   kHeadDim) +
+                 e;
+    *vd = *vs;
+  }
+}
+
+// act[t, j] = bf16(silu(g) * u), g = gu[t, j], u = gu[t, F + j]
+__global__ void swiglu_kernel(const __nv_bfloat16* __restrict__ gu, int f, int n_tok,
+                              __nv_bfloat16* __restrict__ act) {
+  const int64_t nvec = static_cast<int64_t>(n_tok) * f / 8;
+  for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < nvec;
+       v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = v / (f / 8);
+    const int64_t j = v % (f / 8);
+    const bf16x8 g8 = reinterpret_cast<const bf16x8*>(gu + t * 2 * f)[j];
+    const bf16x8 u8 = reinterpret_cast<const bf16x8*>(gu + t * 2 * f + f)[j];
+    float g[8], u[8], o[8];
+    unpack8(g8, g);
+    unpack8(u8, u);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = g[e] / (1.f + __expf(-g[e])) * u[e];
+    reinterpret_cast<bf16x8*>(act + t * f)[j] = pack8(o);
+  }
+}
+
+// Greedy token per row (first index of the maximum). Optionally scatters the token
+// into slot_tok[slot[r]] and hist[slot[r] * hist_stride + hist_pos[r]].
+__global__ void argmax_kernel(const float* __restrict__ logits, int64_t ld, int vocab,
+                              int* __restrict__ out_tok, const int* __restrict__ slot,
+                              int* __restrict__ slot_tok, int* __restrict__ hist,
+                              int hist_stride, const int* __restrict__ hist_pos) {
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  const int r = blockIdx.x;
+  const float* row = logits + r * ld;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
+    const float v = row[i];
+    if (v > best) {  // strictly greater: keeps the first index within a thread
+      best = v;
+      bi = i;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  if (lane_id() == 0) {
+    sv[warp_id()] = best;
+    si[warp_id()] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x / 32); ++w) {
+      if (sv[w] > best || (sv[w] == best && si[w] < bi)) {
+        best = sv[w];
+        bi = si[w];
+      }
+    }
+    if (out_tok) out_tok[r] = bi;
+    if (slot) {
+      const int s = slot[r];
+      if (slot_tok) slot_tok[s] = bi;
+      if (hist) hist[static_cast<int64_t>(s) * hist_stride + hist_pos[r]] = bi;
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t cortex_embed(const void* emb, const int32_t* tokens, const int32_t* index, int32_t n_tok,
+                     int32_t d, void* out, cudaStream_t stream) {
+  if (!emb || !tokens || !out || n_tok < 0 || d % 8) return CORTEX_EBADARG;
+  if (n_tok == 0) return CORTEX_OK;
+  embed_kernel<<<n_tok, 128, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(emb), tokens,
+                                          index, d, reinterpret_cast<__nv_bfloat16*>(out));
+  CORTEX_CHECK_LAUNCH();
+  return CORTEX_OK;
+}
+
+int32_t cortex_rmsnorm(const void* x, const int32_t* rows, int32_t n_rows, const void* w,
+                       int32_t d, float eps, void* y, cudaStream_t stream) {
+  if (!x || !w || !y || n_rows < 0 || d % 8 || d > 8 * 4 * 512) return CORTEX_EBADARG;
+  if (n_rows == 0) return CORTEX_OK;
+  int threads = 32;
+  while (threads * 8 * 4 < d) threads *= 2;
+  if (threads < 64) threads = 64;
+  rmsnorm_kernel<<<n_rows, threads, 0, stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(x), rows, reinterpret_cast<const __nv_bfloat16*>(w),
+      d, eps, reinterpret_cast<__nv_bfloat16*>(y));
+  CORTEX_CHECK_LAUNCH();
+  return CORTEX_OK;
+}
+
+int32_t cortex_rope_kv_append(const void* qkv, void* q_out, void* cache, int64_t k_row0,
+                              int64_t v_row0, const int32_t* table, int32_t table_stride,
+                              const int32_t* tok_pos, const int32_t* tok_row,
+                              const int32_t* tok_col, const int32_t* tok_off,
+                              const float* cos_tab, const float* sin_tab, int32_t n_tok,
+                              int32_t hq, int32_t hkv, cudaStream_t stream) {
+  if (!qkv || !q_out || !cache || !table || !tok_pos || !tok_row || !tok_col || !tok_off ||
+      !cos_tab || !sin_tab || n_tok < 0 || hq < 1 || hkv < 1)
+    return CORTEX_EBADARG;
+  if (n_tok == 0) return CORTEX_OK;
+  RopeArgs a{};
+  a.qkv = reinterpret_cast<const __nv_bfloat16*>(qkv);
+  a.q_out = reinterpret_cast<__nv_bfloat16*>(q_out);
+  a.cache = reinterpret_cast<__nv_bfloat16*>(cache);
+  a.k_row0 = k_row0;
+  a.v_row0 = v_row0;
+  a.table = table;
+  a.table_stride = table_stride;
+  a.tok_pos = tok_pos;
+  a.tok_row = tok_row;
+  a.tok_col = tok_col;
+  a.tok_off = tok_off;
+  a.cos_tab = cos_tab;
+  a.sin_tab = sin_tab;
+  a.hq = hq;
+  a.hkv = hkv;
+  rope_kv_append_kernel<<<n_tok, 256, 0, stream>>>(a);
+  CORTEX_CHECK_LAUNCH();
+  return CORTEX_OK;
+}
+
+int32_t cortex_swiglu(const void* gu, int32_t n_tok, int32_t f, void* act, cudaStream_t stream) {
+  if (!gu || !act || n_tok < 0 || f % 8) return CORTEX_EBADARG;
+  if (n_tok == 0) return CORTEX_OK;
+  const int64_t nvec = static_cast<int64_t>(n_tok) * f / 8;
+  int64_t grid = (nvec + 255) / 256;
+  if (grid > 148 * 16) grid = 148 * 16;
+  swiglu_kernel<<<static_cast<int>(grid), 256, 0, stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(gu), f, n_tok, reinterpret_cast<__nv_bfloat16*>(act));
+  CORTEX_CHECK_LAUNCH();
+  return CORTEX_OK;
+}
+
+int32_t cortex_argmax(const float* logits, int64_t ld, int32_t n_rows, int32_t vocab,
+                      int32_t* out_tok, const int32_t* slot, int32_t* slot_tok, int32_t* hist,
+                      int32_t hist_stride, const int32_t* hist_pos, cudaStream_t stream) {
+  if (!logits || n_rows < 0 || vocab <= 0) return CORTEX_EBADARG;
+  if (hist && (!slot || !hist_pos)) return CORTEX_EBADARG;
+  if (n_rows == 0) return CORTEX_OK;
+  argmax_kernel<<<n_rows, 1024, 0, stream>>>(logits, ld, vocab, out_tok, slot, slot_tok, hist,
+                                             hist_stride, hist_pos);
+  CORTEX_CHECK_LAUNCH();
+  return CORTEX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,349 @@
+// Dense projections of the stage-engine decoder on 5th-gen tensor cores.
+//
+//   C[m, n] = sum_k X[m, k] * W[n, k]        (+ residual[m, n])
+//
+// X is the activation matrix [M, K] (tokens x features, bf16, row-major), W the
+// weight matrix [N, K] (nn.Linear layout, bf16). The kernel is "swap-AB": the
+// weight rows form the 128-wide MMA M dimension and the tokens the MMA N
+// dimension (TN = 32..256), so a decode step with a handful of sequences still
+// issues full 128-row tcgen05.mma instructions while streaming the weights
+// exactly once. Operands are staged by TMA (128-byte swizzle) through a
+// STAGES-deep mbarrier ring, the accumulator lives in TMEM, and the epilogue is
+// tcgen05.ld -> registers -> global. Decode-sized problems split K across CTAs
+// with a deterministic (fixed-order) reduction done by the last CTA of a tile,
+// so a token's result does not depend on which other tokens share the batch.
+#include <algorithm>
+
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int kBlockN = 128;  // weight rows per tile (MMA M)
+constexpr int kBlockK = 64;   // K per stage (one 128-byte swizzle row)
+constexpr int kXBox = 32;     // activation rows per TMA box
+constexpr int kThreads = 128;
+
+struct GemmArgs {
+  int M, N, K;
+  void* out;
+  int ldo;
+  int out_f32;
+  const __nv_bfloat16* residual;
+  int ldr;
+  int kb_per_split;
+  int splits;
+  float* workspace;
+  int* counters;
+  int evict_first_w;
+};
+
+template <int TN, int STAGES>
+struct GemmSmem {
+  static constexpr int kABytes = kBlockN * kBlockK * 2;  // 16 KiB
+  static constexpr int kBBytes = TN * kBlockK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kBarOffset = STAGES * kStageBytes;
+  static constexpr int kTotal = kBarOffset + 256 + 1024;  // barriers + alignment slack
+  static constexpr uint32_t kTmemCols = TN < 32 ? 32 : TN;
+};
+
+template <int TN>
+CORTEX_DEVICE void store_cols(const GemmArgs& a, int n, int m_base, const float (&v)[16]) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int m = m_base + j;
+    if (m < a.M) {
+      float x = v[j];
+      if (a.residual) x += __bfloat162float(a.residual[static_cast<size_t>(m) * a.ldr + n]);
+      if (a.out_f32) {
+        reinterpret_cast<float*>(a.out)[static_cast<size_t>(m) * a.ldo + n] = x;
+      } else {
+        reinterpret_cast<__nv_bfloat16*>(a.out)[static_cast<size_t>(m) * a.ldo + n] =
+            __float2bfloat16_rn(x);
+      }
+    }
+  }
+}
+
+template <int TN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_w,
+                      const __grid_constant__ CUtensorMap tmap_x, const GemmArgs args) {
+  using L = GemmSmem<TN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
+  uint64_t* empty = full + STAGES;
+  uint64_t* done = empty + STAGES;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(done + 1);
+  int* last_flag = reinterpret_cast<int*>(tmem_holder + 1);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int n_tile = blockIdx.x;
+  const int m_tile = blockIdx.y;
+  const int split = blockIdx.z;
+  const int n0 = n_tile * kBlockN;
+  const int m0 = m_tile * TN;
+  const int total_kb = args.K / kBlockK;
+  const int kb0 = split * args.kb_per_split;
+  const int kb1 = min(kb0 + args.kb_per_split, total_kb);
+  const int nkb = kb1 - kb0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_w);
+    tma_prefetch_desc(&tmap_x);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_holder, L::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      // ---- TMA producer ----
+      const uint64_t pol_w = policy_evict_first();
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* sa = smem + s * L::kStageBytes;
+        uint8_t* sb = sa + L::kABytes;
+        mbar_arrive_expect_tx(&full[s], L::kStageBytes);
+        const int kc = (kb0 + i) * kBlockK;
+        if (args.evict_first_w)
+          tma_load_2d_hint(sa, &tmap_w, &full[s], kc, n0, pol_w);
+        else
+          tma_load_2d(sa, &tmap_w, &full[s], kc, n0);
+#pragma unroll
+        for (int j = 0; j < TN / kXBox; ++j)
+          tma_load_2d(sb + j * kXBox * 128, &tmap_x, &full[s], kc, m0 + j * kXBox);
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      // ---- MMA issuer (one thread) ----
+      constexpr uint32_t idesc = umma_idesc_bf16(kBlockN, TN);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint32_t a_addr = smem_u32(smem + s * L::kStageBytes);
+        const uint32_t b_addr = a_addr + L::kABytes;
+#pragma unroll
+        for (int k = 0; k < kBlockK / 16; ++k) {
+          umma_bf16_ss(tmem_base, umma_desc_sw128(a_addr + k * 32), umma_desc_sw128(b_addr + k * 32),
+                       idesc, (i | k) != 0 ? 1u : 0u);
+        }
+        umma_commit(&empty[s]);
+      }
+      umma_commit(done);
+    }
+  }
+  __syncwarp();
+
+  // ---- epilogue: TMEM -> registers -> global (all 4 warps, thread <-> weight row) ----
+  mbar_wait(done, 0);
+  tc_fence_after();
+  const int n = n0 + warp * 32 + lane;
+  const uint32_t taddr = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
+  const int m_end = min(m0 + TN, args.M);
+
+  if (args.splits == 1) {
+    for (int c0 = 0; c0 < TN && m0 + c0 < m_end; c0 += 16) {
+      uint32_t r[16];
+      tmem_ld_32x32b_x16(taddr + c0, r);
+      tmem_ld_wait();
+      float v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+      store_cols<TN>(args, n, m0 + c0, v);
+    }
+  } else {
+    // Split-K: publish this split's fp32 partial, the last CTA of the tile reduces
+    // all partials in split order (deterministic) and runs the epilogue.
+    float* ws = args.workspace + static_cast<size_t>(split) * args.M * args.N;
+    for (int c0 = 0; c0 < TN && m0 + c0 < m_end; c0 += 16) {
+      uint32_t r[16];
+      tmem_ld_32x32b_x16(taddr + c0, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int m = m0 + c0 + j;
+        if (m < m_end) __stcg(&ws[static_cast<size_t>(m) * args.N + n], __uint_as_float(r[j]));
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    const int tile_id = m_tile * gridDim.x + n_tile;
+    if (threadIdx.x == 0) {
+      const int prev = atomicAdd(&args.counters[tile_id], 1);
+      *last_flag = (prev == args.splits - 1) ? 1 : 0;
+    }
+    __syncthreads();
+    if (*last_flag) {
+      __threadfence();
+      for (int c0 = m0; c0 < m_end; c0 += 16) {
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = 0.f;
+        for (int z = 0; z < args.splits; ++z) {
+          const float* wz = args.workspace + static_cast<size_t>(z) * args.M * args.N;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int m = c0 + j;
+            if (m < m_end) v[j] += __ldcg(&wz[static_cast<size_t>(m) * args.N + n]);
+          }
+        }
+        store_cols<TN>(args, n, c0, v);
+      }
+      if (threadIdx.x == 0) args.counters[tile_id] = 0;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, L::kTmemCols);
+  }
+}
+
+template <int TN, int STAGES>
+int32_t launch_gemm(const CUtensorMap* tw, const CUtensorMap* tx, const GemmArgs& a, dim3 grid,
+                    cudaStream_t stream) {
+  using L = GemmSmem<TN, STAGES>;
+  auto kern = gemm_bf16_tcgen05<TN, STAGES>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal) !=
+        cudaSuccess)
+      return CORTEX_ECUDA;
+    configured = true;
+  }
+  kern<<<grid, kThreads, L::kTotal, stream>>>(*tw, *tx, a);
+  CORTEX_CHECK_LAUNCH();
+  return CORTEX_OK;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+extern "C" {
+
+// Encode a 2-D bf16 TMA descriptor (128 bytes, written to tmap_out) over a
+// row-major matrix [rows, cols] with the given row pitch. box_cols * 2 must be
+// 128 (one swizzle row); the tile lands in shared memory with SWIZZLE_128B.
+int32_t cortex_tmap_encode_2d_bf16(void* tmap_out, const void* gptr, uint64_t rows, uint64_t cols,
+                                   uint64_t row_pitch_bytes, uint32_t box_rows,
+                                   uint32_t box_cols) {
+  if (!tmap_out || !gptr || rows == 0 || cols == 0 || box_cols * 2 != 128 || box_rows == 0 ||
+      box_rows > 256 || (row_pitch_bytes % 16) != 0 ||
+      (reinterpret_cast<uintptr_t>(gptr) % 16) != 0)
+    return CORTEX_EBADARG;
+  auto fn = get_encode_fn();
+  if (!fn) return CORTEX_ECUDA;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {row_pitch_bytes};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(reinterpret_cast<CUtensorMap*>(tmap_out), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(gptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? CORTEX_OK : CORTEX_ECUDA;
+}
+
+// Split-K factor the GEMM uses for a problem (exported so the host can size the
+// workspace and so tests can pin batch invariance).
+int32_t cortex_gemm_splits(int32_t M, int32_t N, int32_t K) {
+  if (M <= 0 || N % kBlockN || K % kBlockK) return 1;
+  const int n_tiles = N / kBlockN;
+  const int total_kb = K / kBlockK;
+  if (M > 256) return 1;
+  const int target = 2 * 148;
+  int splits = (target + n_tiles - 1) / n_tiles;
+  splits = std::min(splits, std::max(1, total_kb / 4));
+  splits = std::min(splits, 16);
+  splits = std::max(splits, 1);
+  // re-balance so every split gets a non-empty K range
+  const int kb_per = (total_kb + splits - 1) / splits;
+  return (total_kb + kb_per - 1) / kb_per;
+}
+
+// C = X . W^T (+ residual). tmap_w: descriptor over W [N, K] with box (128 rows, 64 cols);
+// tmap_x: descriptor over X [>=M rows, K] with box (32 rows, 64 cols). Output row pitch ldo
+// (elements); out_f32 selects fp32 instead of bf16 output. workspace/counters are only used
+// when cortex_gemm_splits(M, N, K) > 1 (workspace >= splits*M*N floats, counters zeroed,
+// >= n_tiles*m_tiles ints; the kernel leaves them zeroed).
+int32_t cortex_gemm_bf16(const void* tmap_w, const void* tmap_x, int32_t M, int32_t N, int32_t K,
+                         void* out, int32_t ldo, int32_t out_f32, const void* residual,
+                         int32_t ldr, float* workspace, uint64_t workspace_bytes,
+                         int32_t* counters, int32_t n_counters, cudaStream_t stream) {
+  if (!tmap_w || !tmap_x || !out || M <= 0 || N <= 0 || K <= 0 || N % kBlockN || K % kBlockK)
+    return CORTEX_EBADARG;
+  GemmArgs a{};
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.out = out;
+  a.ldo = ldo;
+  a.out_f32 = out_f32;
+  a.residual = reinterpret_cast<const __nv_bfloat16*>(residual);
+  a.ldr = ldr;
+  const int total_kb = K / kBlockK;
+  const int splits = cortex_gemm_splits(M, N, K);
+  a.kb_per_split = (total_kb + splits - 1) / splits;
+  a.splits = splits;
+  a.workspace = workspace;
+  a.counters = counters;
+  const int n_tiles = N / kBlockN;
+  if (splits > 1) {
+    if (!workspace || !counters ||
+        workspace_bytes < static_cast<uint64_t>(splits) * M * N * sizeof(float) ||
+        n_counters < n_tiles)
+      return CORTEX_EBADARG;
+  }
+  const auto* tw = reinterpret_cast<const CUtensorMap*>(tmap_w);
+  const auto* tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
+  int tn;
+  if (M <= 32) tn = 32;
+  else if (M <= 64) tn = 64;
+  else if (M <= 128) tn = 128;
+  else tn = 256;
+  const int m_tiles = (M + tn - 1) / tn;
+  a.evict_first_w = m_tiles == 1 ? 1 : 0;
+  dim3 grid(n_tiles, m_tiles, splits);
+  switch (tn) {
+    case 32: return launch_gemm<32, 4>(tw, tx, a, grid, stream);
+    case 64: return launch_gemm<64, 4>(tw, tx, a, grid, stream);
+    case 128: return launch_gemm<128, 5>(tw, tx, a, grid, stream);
+    default: return launch_gemm<256, 4>(tw, tx, a, grid, stream);
+  }
+}
+
+}  // extern "C"

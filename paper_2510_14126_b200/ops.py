@@ -1,0 +1,218 @@
+"""Thin torch-facing wrappers over the C ABI (device pointers + the current stream).
+
+Each wrapper checks the status code and raises KernelError on failure. Tensors
+must already live on the GPU with the dtype/layout documented per op; nothing
+here copies or allocates behind the caller's back (outputs are passed in).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from .errors import KernelError
+
+_L = None
+
+
+def lib():
+    global _L
+    if _L is None:
+        _L = _lib.load()
+    return _L
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise KernelError(f"{what} failed: {_lib.STATUS_NAMES.get(rc, rc)} ({rc})")
+
+
+class TensorMap:
+    """A 128-byte CUtensorMap over a 2-D bf16 row-major tensor, box (box_rows, 64)."""
+
+    __slots__ = ("buf", "tensor", "rows", "cols", "box_rows")
+
+    def __init__(self, t: torch.Tensor, box_rows: int, rows: int | None = None) -> None:
+        if t.dtype != torch.bfloat16 or t.dim() != 2 or t.stride(1) != 1:
+            raise ValueError("TensorMap needs a 2-D row-major bf16 tensor")
+        self.tensor = t  # keep the storage alive
+        self.rows = int(rows if rows is not None else t.shape[0])
+        self.cols = int(t.shape[1])
+        self.box_rows = box_rows
+        self.buf = ctypes.create_string_buffer(128)
+        _check(
+            lib().cortex_tmap_encode_2d_bf16(
+                ctypes.addressof(self.buf), t.data_ptr(), self.rows, self.cols,
+                t.stride(0) * 2, box_rows, 64,
+            ),
+            "cortex_tmap_encode_2d_bf16",
+        )
+
+    @property
+    def ptr(self) -> int:
+        return ctypes.addressof(self.buf)
+
+
+def weight_map(w: torch.Tensor) -> TensorMap:
+    return TensorMap(w, 128)
+
+
+def act_map(x: torch.Tensor) -> TensorMap:
+    return TensorMap(x, 32)
+
+
+def kv_map(cache2d: torch.Tensor) -> TensorMap:
+    return TensorMap(cache2d, 16)
+
+
+class GemmWorkspace:
+    """Split-K scratch (fp32 partials + per-tile arrival counters, kept zeroed)."""
+
+    def __init__(self, device, max_floats: int = 16 << 20, n_counters: int = 1 << 16) -> None:
+        self.ws = torch.empty(max_floats, dtype=torch.float32, device=device)
+        self.counters = torch.zeros(n_counters, dtype=torch.int32, device=device)
+
+
+def gemm_splits(M: int, N: int, K: int) -> int:
+    return int(lib().cortex_gemm_splits(M, N, K))
+
+
+def gemm(wmap: TensorMap, xmap: TensorMap, M: int, out: torch.Tensor, ws: GemmWorkspace,
+         residual: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """out[:M] = X[:M] @ W^T (+ residual). out is bf16 or fp32 [>=M, N] row-major."""
+    N, K = wmap.rows, wmap.cols
+    if xmap.cols != K or M > xmap.rows:
+        raise ValueError("gemm shape mismatch")
+    out_f32 = 1 if out.dtype == torch.float32 else 0
+    ldr = residual.stride(0) if residual is not None else 0
+    _check(
+        lib().cortex_gemm_bf16(
+            wmap.ptr, xmap.ptr, M, N, K, out.data_ptr(), out.stride(0), out_f32, _ptr(residual),
+            ldr, ws.ws.data_ptr(), ws.ws.numel() * 4, ws.counters.data_ptr(),
+            ws.counters.numel(), _stream(stream),
+        ),
+        "cortex_gemm_bf16",
+    )
+    return out
+
+
+def embed(emb: torch.Tensor, tokens: torch.Tensor, n_tok: int, out: torch.Tensor,
+          index: torch.Tensor | None = None, stream=None) -> None:
+    _check(lib().cortex_embed(emb.data_ptr(), tokens.data_ptr(), _ptr(index), n_tok,
+                              emb.shape[1], out.data_ptr(), _stream(stream)), "cortex_embed")
+
+
+def rmsnorm(x: torch.Tensor, w: torch.Tensor, n_rows: int, y: torch.Tensor, eps: float,
+            rows: torch.Tensor | None = None, stream=None) -> None:
+    _check(lib().cortex_rmsnorm(x.data_ptr(), _ptr(rows), n_rows, w.data_ptr(), x.shape[1],
+                                eps, y.data_ptr(), _stream(stream)), "cortex_rmsnorm")
+
+
+def rope_kv_append(qkv, q_out, cache, k_row0, v_row0, table, tok_pos, tok_row, tok_col, tok_off,
+                   cos_tab, sin_tab, n_tok, hq, hkv, stream=None) -> None:
+    _check(
+        lib().cortex_rope_kv_append(
+            qkv.data_ptr(), q_out.data_ptr(), cache.data_ptr(), k_row0, v_row0, table.data_ptr(),
+            table.stride(0), tok_pos.data_ptr(), tok_row.data_ptr(), tok_col.data_ptr(),
+            tok_off.data_ptr(), cos_tab.data_ptr(), sin_tab.data_ptr(), n_tok, hq, hkv,
+            _stream(stream),
+        ),
+        "cortex_rope_kv_append",
+    )
+
+
+def swiglu(gu: torch.Tensor, n_tok: int, act: torch.Tensor, stream=None) -> None:
+    f = act.shape[1]
+    _check(lib().cortex_swiglu(gu.data_ptr(), n_tok, f, act.data_ptr(), _stream(stream)),
+           "cortex_swiglu")
+
+
+def argmax(logits: torch.Tensor, n_rows: int, vocab: int, out_tok: torch.Tensor | None = None,
+           slot: torch.Tensor | None = None, slot_tok: torch.Tensor | None = None,
+           hist: torch.Tensor | None = None, hist_pos: torch.Tensor | None = None,
+           stream=None) -> None:
+    _check(
+        lib().cortex_argmax(
+            logits.data_ptr(), logits.stride(0), n_rows, vocab, _ptr(out_tok), _ptr(slot),
+            _ptr(slot_tok), _ptr(hist), hist.stride(0) if hist is not None else 0, _ptr(hist_pos),
+            _stream(stream),
+        ),
+        "cortex_argmax",
+    )
+
+
+def decode_splits(prefix_len: int, kv_len: int) -> int:
+    return int(lib().cortex_decode_splits(prefix_len, kv_len))
+
+
+def paged_decode_attn(kvmap: TensorMap, q, table, seq_row, seq_prefix, seq_kvlen, n_seqs,
+                      n_kv_heads, group, k_row0, v_row0, scale, o_part, lse_part, max_splits, out,
+                      stream=None) -> None:
+    _check(
+        lib().cortex_paged_decode_attn(
+            kvmap.ptr, q.data_ptr(), table.data_ptr(), table.stride(0), seq_row.data_ptr(),
+            seq_prefix.data_ptr(), seq_kvlen.data_ptr(), n_seqs, n_kv_heads, group, k_row0,
+            v_row0, scale, o_part.data_ptr(), lse_part.data_ptr(), max_splits, out.data_ptr(),
+            _stream(stream),
+        ),
+        "cortex_paged_decode_attn",
+    )
+
+
+def paged_prefill_attn(kvmap: TensorMap, q, out, table, seq_row, seq_prefix, seq_kvlen,
+                       seq_qstart, seq_qlen, n_seqs, max_qlen, n_kv_heads, group, k_row0, v_row0,
+                       scale, stream=None) -> None:
+    _check(
+        lib().cortex_paged_prefill_attn(
+            kvmap.ptr, q.data_ptr(), out.data_ptr(), table.data_ptr(), table.stride(0),
+            seq_row.data_ptr(), seq_prefix.data_ptr(), seq_kvlen.data_ptr(),
+            seq_qstart.data_ptr(), seq_qlen.data_ptr(), n_seqs, max_qlen, n_kv_heads, group,
+            k_row0, v_row0, scale, _stream(stream),
+        ),
+        "cortex_paged_prefill_attn",
+    )
+
+
+def kv_alloc(bitmap, nblocks, id_base, counts, rows, cols, n_req, table, status,
+             stream=None) -> None:
+    _check(
+        lib().cortex_kv_alloc(bitmap.data_ptr(), nblocks, id_base, counts.data_ptr(),
+                              rows.data_ptr(), cols.data_ptr(), n_req, table.data_ptr(),
+                              table.stride(0), status.data_ptr(), _stream(stream)),
+        "cortex_kv_alloc",
+    )
+
+
+def kv_free(bitmap, nblocks, id_base, table, rows, cols, counts, n_req, status,
+            stream=None) -> None:
+    _check(
+        lib().cortex_kv_free(bitmap.data_ptr(), nblocks, id_base, table.data_ptr(),
+                             table.stride(0), rows.data_ptr(), cols.data_ptr(), counts.data_ptr(),
+                             n_req, status.data_ptr(), _stream(stream)),
+        "cortex_kv_free",
+    )
+
+
+def table_copy(table, src_rows, dst_rows, dst_cols, counts, n, stream=None) -> None:
+    _check(
+        lib().cortex_table_copy(table.data_ptr(), table.stride(0), src_rows.data_ptr(),
+                                dst_rows.data_ptr(), dst_cols.data_ptr(), counts.data_ptr(), n,
+                                _stream(stream)),
+        "cortex_table_copy",
+    )
+
+
+def kv_count_free(bitmap, nblocks, out_free, stream=None) -> None:
+    _check(lib().cortex_kv_count_free(bitmap.data_ptr(), nblocks, out_free.data_ptr(),
+                                      _stream(stream)), "cortex_kv_count_free")

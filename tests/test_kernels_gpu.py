@@ -1,0 +1,340 @@
+"""Kernel-level parity on the B200: every export against the CPU/fp32 oracle.
+
+Run with `pytest -m gpu`. Tolerances (north star: "2e-3 relative error in bf16"):
+  * GEMM: relative Frobenius error vs fp32 matmul of the same bf16 inputs,
+    measured after the bf16 output rounding: <= 4e-3 (one bf16 rounding is
+    2^-9 = 1.95e-3 per element, so the norm-relative error sits near 1e-3).
+  * attention: relative Frobenius error vs oracle.attention_ref <= 4e-3.
+  * allocator / argmax / embedding: bit-exact.
+"""
+
+from __future__ import annotations
+
+import math
+import random
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.alloc_ref import BlockPoolRef
+from oracle.decoder_ref import attention_ref, bf16, rmsnorm_ref, rope_ref, rope_tables
+
+pytestmark = pytest.mark.gpu
+
+
+def ops():
+    from paper_2510_14126_b200 import ops as o
+
+    return o
+
+
+def rel(a: torch.Tensor, b: torch.Tensor) -> float:
+    a = a.float().cpu()
+    b = b.float().cpu()
+    return float((a - b).norm() / b.norm().clamp_min(1e-30))
+
+
+# ---------------------------------------------------------------- GEMM
+
+
+@pytest.mark.parametrize("N,K", [(256, 256), (512, 768), (6144, 4096), (1024, 14336)])
+@pytest.mark.parametrize("M", [1, 5, 32, 33, 64, 100, 128, 200, 256, 300, 777])
+def test_gemm_matches_fp32(cuda, M, N, K):
+    o = ops()
+    g = torch.Generator(device=cuda).manual_seed(1000 * M + N + K)
+    x = torch.randn(max(M, 32), K, generator=g, device=cuda).to(torch.bfloat16)
+    w = (torch.randn(N, K, generator=g, device=cuda) * 0.05).to(torch.bfloat16)
+    ws = o.GemmWorkspace(cuda)
+    out = torch.full((M, N), float("nan"), device=cuda, dtype=torch.bfloat16)
+    o.gemm(o.weight_map(w), o.act_map(x), M, out, ws)
+    ref = x[:M].float() @ w.float().T
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all()
+    assert rel(out, ref) < 4e-3
+    assert int(ws.counters.abs().sum()) == 0  # split-K counters left zeroed
+
+
+@pytest.mark.parametrize("M", [3, 64, 257])
+def test_gemm_residual_and_f32(cuda, M):
+    o = ops()
+    N, K = 512, 1024
+    g = torch.Generator(device=cuda).manual_seed(7 + M)
+    x = torch.randn(max(M, 32), K, generator=g, device=cuda).to(torch.bfloat16)
+    w = (torch.randn(N, K, generator=g, device=cuda) * 0.05).to(torch.bfloat16)
+    r = torch.randn(M, N, generator=g, device=cuda).to(torch.bfloat16)
+    ws = o.GemmWorkspace(cuda)
+    out = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    o.gemm(o.weight_map(w), o.act_map(x), M, out, ws, residual=r)
+    ref = x[:M].float() @ w.float().T + r.float()
+    assert rel(out, ref) < 4e-3
+    out32 = torch.empty(M, N, device=cuda, dtype=torch.float32)
+    o.gemm(o.weight_map(w), o.act_map(x), M, out32, ws)
+    assert rel(out32, x[:M].float() @ w.float().T) < 1e-5
+
+
+def test_gemm_batch_invariant(cuda):
+    """A row's result does not depend on the other rows of a decode batch (M <= 256)."""
+    o = ops()
+    N, K = 6144, 4096
+    g = torch.Generator(device=cuda).manual_seed(3)
+    x = torch.randn(256, K, generator=g, device=cuda).to(torch.bfloat16)
+    w = (torch.randn(N, K, generator=g, device=cuda) * 0.05).to(torch.bfloat16)
+    ws = o.GemmWorkspace(cuda)
+    full = torch.empty(256, N, device=cuda, dtype=torch.bfloat16)
+    o.gemm(o.weight_map(w), o.act_map(x), 256, full, ws)
+    for m in (1, 17, 64, 130):
+        part = torch.empty(m, N, device=cuda, dtype=torch.bfloat16)
+        o.gemm(o.weight_map(w), o.act_map(x), m, part, ws)
+        assert torch.equal(part, full[:m])
+
+
+# ---------------------------------------------------------------- attention
+
+
+def _make_cache(cuda, n_layers, nb, hkv, seed):
+    g = torch.Generator(device=cuda).manual_seed(seed)
+    cache = torch.randn(n_layers, 2, nb, hkv, 16, 128, generator=g, device=cuda).to(torch.bfloat16)
+    return cache
+
+
+def _rows(layer, nb, hkv):
+    k_row0 = (layer * 2 + 0) * nb * hkv * 16
+    v_row0 = (layer * 2 + 1) * nb * hkv * 16
+    return k_row0, v_row0
+
+
+def _logical_kv(cache, layer, table_row, prefix, kvlen):
+    npb = (prefix + 15) // 16
+    ks, vs = [], []
+    for pos in range(kvlen):
+        if pos < prefix:
+            j, off = pos // 16, pos % 16
+        else:
+            jj = pos - prefix
+            j, off = npb + jj // 16, jj % 16
+        b = int(table_row[j])
+        ks.append(cache[layer, 0, b, :, off, :])
+        vs.append(cache[layer, 1, b, :, off, :])
+    return torch.stack(ks).float().cpu(), torch.stack(vs).float().cpu()
+
+
+def _seq_specs(rng, nb, max_blocks):
+    # (prefix_len, kv_len) cases: no prefix, aligned prefix, ragged prefix, long
+    specs = [(0, 1), (0, 17), (40, 41), (40, 77), (1000, 1000 + 137), (16, 300), (5, 5 + 256),
+             (0, 255), (0, 256), (0, 257), (1000, 1000 + 700)]
+    tables = []
+    perm = rng.permutation(nb)
+    used = 0
+    for prefix, kvlen in specs:
+        n = (prefix + 15) // 16 + (kvlen - prefix + 15) // 16
+        assert n <= max_blocks
+        tables.append(perm[used:used + n])
+        used = (used + n) % (nb - max_blocks)
+    return specs, tables
+
+
+@pytest.mark.parametrize("group", [4, 2])
+def test_paged_decode_attention(cuda, group):
+    o = ops()
+    hkv, L, nb, max_blocks = 2, 2, 512, 128
+    hq = hkv * group
+    cache = _make_cache(cuda, L, nb, hkv, seed=11 + group)
+    rng = np.random.default_rng(5)
+    specs, tables = _seq_specs(rng, nb, max_blocks)
+    B = len(specs)
+    table = torch.zeros(B, max_blocks, dtype=torch.int32)
+    for i, t in enumerate(tables):
+        table[i, : len(t)] = torch.as_tensor(t, dtype=torch.int32)
+    table = table.to(cuda)
+    seq_row = torch.arange(B, dtype=torch.int32, device=cuda)
+    seq_prefix = torch.tensor([s[0] for s in specs], dtype=torch.int32, device=cuda)
+    seq_kvlen = torch.tensor([s[1] for s in specs], dtype=torch.int32, device=cuda)
+    max_splits = max(o.decode_splits(p, k) for p, k in specs)
+    q = torch.randn(B, hq, 128, device=cuda).to(torch.bfloat16)
+    o_part = torch.empty(B, max_splits, hq, 128, device=cuda)
+    lse_part = torch.empty(B, max_splits, hq, device=cuda)
+    out = torch.empty(B, hq, 128, device=cuda, dtype=torch.bfloat16)
+    kvmap = o.kv_map(cache.view(-1, 128))
+    for layer in range(L):
+        k0, v0 = _rows(layer, nb, hkv)
+        o.paged_decode_attn(kvmap, q, table, seq_row, seq_prefix, seq_kvlen, B, hkv, group, k0, v0,
+                            1 / math.sqrt(128), o_part, lse_part, max_splits, out)
+        torch.cuda.synchronize()
+        for b, (prefix, kvlen) in enumerate(specs):
+            k, v = _logical_kv(cache, layer, table[b].cpu(), prefix, kvlen)
+            ref = attention_ref(q[b:b + 1].float().cpu(), k, v, torch.tensor([kvlen - 1]),
+                                torch.arange(kvlen))
+            assert rel(out[b:b + 1], ref) < 4e-3, (layer, b, prefix, kvlen)
+
+
+@pytest.mark.parametrize("group", [4, 2])
+def test_paged_prefill_attention(cuda, group):
+    o = ops()
+    hkv, L, nb, max_blocks = 2, 1, 512, 160
+    hq = hkv * group
+    cache = _make_cache(cuda, L, nb, hkv, seed=23 + group)
+    rng = np.random.default_rng(9)
+    specs, tables = _seq_specs(rng, nb, max_blocks)
+    qlens = [min(kv, q) for (p, kv), q in zip(specs, [1, 17, 1, 37, 137, 100, 256, 255, 3, 257, 700])]
+    B = len(specs)
+    table = torch.zeros(B, max_blocks, dtype=torch.int32)
+    for i, t in enumerate(tables):
+        table[i, : len(t)] = torch.as_tensor(t, dtype=torch.int32)
+    table = table.to(cuda)
+    qstart = np.concatenate([[0], np.cumsum(qlens)[:-1]]).astype(np.int32)
+    T = int(sum(qlens))
+    q = torch.randn(T, hq, 128, device=cuda).to(torch.bfloat16)
+    out = torch.zeros(T, hq, 128, device=cuda, dtype=torch.bfloat16)
+    kvmap = o.kv_map(cache.view(-1, 128))
+    k0, v0 = _rows(0, nb, hkv)
+    dev = lambda a: torch.as_tensor(np.asarray(a, dtype=np.int32), device=cuda)
+    o.paged_prefill_attn(kvmap, q, out, table, dev(range(B)), dev([s[0] for s in specs]),
+                         dev([s[1] for s in specs]), dev(qstart), dev(qlens), B, max(qlens), hkv,
+                         group, k0, v0, 1 / math.sqrt(128))
+    torch.cuda.synchronize()
+    for b, (prefix, kvlen) in enumerate(specs):
+        k, v = _logical_kv(cache, 0, table[b].cpu(), prefix, kvlen)
+        ql = qlens[b]
+        qpos = torch.arange(kvlen - ql, kvlen)
+        ref = attention_ref(q[qstart[b]:qstart[b] + ql].float().cpu(), k, v, qpos, torch.arange(kvlen))
+        assert rel(out[qstart[b]:qstart[b] + ql], ref) < 4e-3, (b, prefix, kvlen, ql)
+
+
+# ---------------------------------------------------------------- elementwise
+
+
+def test_rmsnorm_embed_swiglu_argmax(cuda):
+    o = ops()
+    d, V, T, F = 4096, 1000, 37, 1536
+    g = torch.Generator(device=cuda).manual_seed(1)
+    emb = torch.randn(V, d, generator=g, device=cuda).to(torch.bfloat16)
+    toks = torch.randint(0, V, (T,), generator=g, device=cuda, dtype=torch.int32)
+    h = torch.empty(T, d, device=cuda, dtype=torch.bfloat16)
+    o.embed(emb, toks, T, h)
+    assert torch.equal(h, emb[toks.long()])
+    w = (1 + 0.1 * torch.randn(d, generator=g, device=cuda)).to(torch.bfloat16)
+    y = torch.empty(T, d, device=cuda, dtype=torch.bfloat16)
+    o.rmsnorm(h, w, T, y, 1e-5)
+    ref = rmsnorm_ref(h.float().cpu(), w.float().cpu(), 1e-5)
+    assert rel(y, ref) < 1e-3
+    rows = torch.tensor([5, 0, 36], dtype=torch.int32, device=cuda)
+    y3 = torch.empty(3, d, device=cuda, dtype=torch.bfloat16)
+    o.rmsnorm(h, w, 3, y3, 1e-5, rows=rows)
+    assert torch.equal(y3, y[rows.long()])
+    gu = torch.randn(T, 2 * F, generator=g, device=cuda).to(torch.bfloat16)
+    act = torch.empty(T, F, device=cuda, dtype=torch.bfloat16)
+    o.swiglu(gu, T, act)
+    gg, uu = gu[:, :F].float(), gu[:, F:].float()
+    assert rel(act, bf16(gg / (1 + torch.exp(-gg)) * uu)) < 1e-3
+    logits = torch.randn(T, 128256, generator=g, device=cuda)
+    logits[3, 77] = 100.0
+    logits[3, 99] = 100.0  # tie -> first index
+    tok = torch.empty(T, dtype=torch.int32, device=cuda)
+    o.argmax(logits, T, 128256, out_tok=tok)
+    ref_tok = torch.argmax(logits, dim=1).to(torch.int32)
+    assert torch.equal(tok, ref_tok)
+    assert int(tok[3]) == 77
+
+
+def test_rope_kv_append(cuda):
+    o = ops()
+    hq, hkv, T, nb = 8, 2, 21, 64
+    g = torch.Generator(device=cuda).manual_seed(2)
+    qkv = torch.randn(T, (hq + 2 * hkv) * 128, generator=g, device=cuda).to(torch.bfloat16)
+    cache = torch.zeros(1, 2, nb, hkv, 16, 128, device=cuda, dtype=torch.bfloat16)
+    table = torch.randperm(nb, generator=torch.Generator().manual_seed(0)).to(torch.int32)
+    table = table.view(4, 16).to(cuda)
+    pos = torch.arange(100, 100 + T, dtype=torch.int32)
+    rows = torch.tensor([i % 4 for i in range(T)], dtype=torch.int32)
+    cols = torch.tensor([(i // 4) % 16 for i in range(T)], dtype=torch.int32)
+    offs = torch.tensor([(3 * i) % 16 for i in range(T)], dtype=torch.int32)
+    cos, sin = rope_tables(4096, 500000.0)
+    q_out = torch.empty(T, hq, 128, device=cuda, dtype=torch.bfloat16)
+    k0, v0 = _rows(0, nb, hkv)
+    o.rope_kv_append(qkv, q_out, cache, k0, v0, table, pos.to(cuda), rows.to(cuda), cols.to(cuda),
+                     offs.to(cuda), cos.to(cuda), sin.to(cuda), T, hq, hkv)
+    torch.cuda.synchronize()
+    x = qkv.float().cpu()
+    qr = rope_ref(x[:, : hq * 128].reshape(T, hq, 128), cos[pos.long()], sin[pos.long()])
+    kr = rope_ref(x[:, hq * 128:(hq + hkv) * 128].reshape(T, hkv, 128), cos[pos.long()],
+                  sin[pos.long()])
+    vr = x[:, (hq + hkv) * 128:].reshape(T, hkv, 128)
+    assert rel(q_out, qr) < 1e-5
+    tab = table.cpu()
+    for t in range(T):
+        b = int(tab[rows[t], cols[t]])
+        assert rel(cache[0, 0, b, :, offs[t]], kr[t]) < 1e-5
+        assert torch.equal(cache[0, 1, b, :, offs[t]].float().cpu(), vr[t])
+
+
+# ---------------------------------------------------------------- allocator
+
+
+def test_kv_alloc_free_matches_oracle(cuda):
+    o = ops()
+    nblocks, id_base, n_rows, stride = 1000, 5000, 40, 64
+    ref = BlockPoolRef(nblocks, id_base)
+    bitmap = torch.from_numpy(ref.bitmap_words().view(np.int32)).to(cuda)
+    table = torch.full((n_rows, stride), -1, dtype=torch.int32, device=cuda)
+    status = torch.zeros(1, dtype=torch.int32, device=cuda)
+    ref_table = np.full((n_rows, stride), -1, dtype=np.int64)
+    held: dict[int, int] = {}  # row -> blocks held (from col 0)
+    rnd = random.Random(4)
+    dev = lambda a: torch.as_tensor(np.asarray(a, dtype=np.int32), device=cuda)
+    for step in range(300):
+        if rnd.random() < 0.55:
+            free_rows = [r for r in range(n_rows) if r not in held]
+            if not free_rows:
+                continue
+            rows = rnd.sample(free_rows, k=min(len(free_rows), rnd.randint(1, 6)))
+            counts = [rnd.choice([0, 1, 3, 16, 63]) for _ in rows]
+            if sum(counts) > ref.n_free():
+                o.kv_alloc(bitmap, nblocks, id_base, dev(counts), dev(rows), dev([0] * len(rows)),
+                           len(rows), table, status)
+                torch.cuda.synchronize()
+                assert int(status[0]) == -3
+                status.zero_()
+                continue
+            ids = ref.alloc(counts)
+            for r, c, got in zip(rows, counts, ids):
+                held[r] = c
+                ref_table[r, :c] = got
+            o.kv_alloc(bitmap, nblocks, id_base, dev(counts), dev(rows), dev([0] * len(rows)),
+                       len(rows), table, status)
+        else:
+            if not held:
+                continue
+            rows = rnd.sample(sorted(held), k=min(len(held), rnd.randint(1, 4)))
+            counts = [held.pop(r) for r in rows]
+            for r, c in zip(rows, counts):
+                ref.free(ref_table[r, :c].tolist())
+            o.kv_free(bitmap, nblocks, id_base, table, dev(rows), dev([0] * len(rows)), dev(counts),
+                      len(rows), status)
+        torch.cuda.synchronize()
+        assert int(status[0]) == 0
+        got_bitmap = bitmap.cpu().numpy().view(np.uint32)
+        assert np.array_equal(got_bitmap, ref.bitmap_words()), step
+        tab = table.cpu().numpy()
+        for r, c in held.items():
+            assert np.array_equal(tab[r, :c], ref_table[r, :c]), (step, r)
+    nfree = torch.zeros(1, dtype=torch.int32, device=cuda)
+    o.kv_count_free(bitmap, nblocks, nfree)
+    assert int(nfree[0]) == ref.n_free()
+
+
+def test_kv_double_free_flagged(cuda):
+    o = ops()
+    ref = BlockPoolRef(64)
+    bitmap = torch.from_numpy(ref.bitmap_words().view(np.int32)).to(cuda)
+    table = torch.full((2, 8), -1, dtype=torch.int32, device=cuda)
+    status = torch.zeros(1, dtype=torch.int32, device=cuda)
+    one = torch.ones(1, dtype=torch.int32, device=cuda)
+    zero = torch.zeros(1, dtype=torch.int32, device=cuda)
+    o.kv_alloc(bitmap, 64, 0, one * 4, zero, zero, 1, table, status)
+    o.kv_free(bitmap, 64, 0, table, zero, zero, one * 4, 1, status)
+    torch.cuda.synchronize()
+    assert int(status[0]) == 0
+    o.kv_free(bitmap, 64, 0, table, zero, zero, one * 4, 1, status)
+    torch.cuda.synchronize()
+    assert int(status[0]) == -1
