@@ -89,7 +89,8 @@ int32_t cortex_tmap_encode_2d_bf16(void* tmap_out, const void* gptr, uint64_t ro
 /* ---- decoder forward (the GPU work behind admit's prefill and
  * advance_decode's emitted tokens) -------------------------------------------- */
 
-/* tcgen05/TMEM GEMM: out[m, n] = sum_k X[m, k] W[n, k] (+ residual[m, n]).
+/* tcgen05/TMEM GEMM: out[m, n] = sum_k X[m, k] W[n, k] (+ residual[m, n], fp32 with row
+ * pitch ldr; the residual stream is fp32, so residual GEMMs use out_f32 = 1).
  * tmap_w over W [N, K] with box (128, 64); tmap_x over X [>= M, K] with box (32, 64).
  * workspace / counters are used when cortex_gemm_splits(M, N, K) > 1. */
 int32_t cortex_gemm_splits(int32_t M, int32_t N, int32_t K);
@@ -98,9 +99,11 @@ int32_t cortex_gemm_bf16(const void* tmap_w, const void* tmap_x, int32_t M, int3
                          int32_t ldr, float* workspace, uint64_t workspace_bytes,
                          int32_t* counters, int32_t n_counters, cortex_stream_t stream);
 
+/* out[t] (fp32, the residual stream) = emb[tokens[index ? index[t] : t]] (bf16 table). */
 int32_t cortex_embed(const void* emb, const int32_t* tokens, const int32_t* index, int32_t n_tok,
                      int32_t d, void* out, cortex_stream_t stream);
 
+/* y[r] (bf16) = x[rows ? rows[r] : r] (fp32) * rsqrt(mean(x^2) + eps) * w (bf16). */
 int32_t cortex_rmsnorm(const void* x, const int32_t* rows, int32_t n_rows, const void* w,
                        int32_t d, float eps, void* y, cortex_stream_t stream);
 

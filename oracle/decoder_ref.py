@@ -15,13 +15,13 @@ Model: Llama-style decoder (RMSNorm, RoPE rotate-half, GQA, SwiGLU, untied
 lm_head). Arithmetic is fp32; every tensor the GPU path stores in bf16 is
 rounded to bf16 at the same point here, so GPU and oracle differ only by fp32
 summation order:
-  h0 = E[tok]
+  h0 = E[tok]                                   (residual stream h is fp32)
   per layer: xn = bf16(h * rsqrt(mean(h^2) + eps) * w_attn)
              qkv = bf16(xn Wqkv^T);  q,k = bf16(rope(q,k));  K/V cache bf16
              a = bf16(softmax(q k^T / sqrt(128)) v)        (causal, fp32)
-             h = bf16(a Wo^T + h)
+             h = a Wo^T + h
              xn = bf16(rmsnorm(h) * w_mlp);  gu = bf16(xn Wgu^T)
-             act = bf16(silu(g) * u);  h = bf16(act Wd^T + h)
+             act = bf16(silu(g) * u);  h = act Wd^T + h
   logits = fp32(bf16(rmsnorm(h) * w_final) Wlm^T);  token = first argmax
 """
 
@@ -138,12 +138,12 @@ class RefSeq:
             self.v[li] = torch.cat([self.v[li], v])
             kpos = torch.arange(self.k[li].shape[0])
             a = attention_ref(q, self.k[li], self.v[li], pos, kpos).reshape(n, hq * HEAD_DIM)
-            h = bf16(a @ w[p + "wo"].T + h)
+            h = a @ w[p + "wo"].T + h
             xn = rmsnorm_ref(h, w[p + "mlp_norm"], c.eps)
             gu = bf16(xn @ w[p + "wgu"].T)
             g, u = gu[:, : c.ffn], gu[:, c.ffn:]
             act = bf16(g / (1.0 + torch.exp(-g)) * u)
-            h = bf16(act @ w[p + "wd"].T + h)
+            h = act @ w[p + "wd"].T + h
         self.length += n
         if want_logits == "none":
             return None

@@ -158,11 +158,14 @@ CORTEX_DEVICE void attend_tile(WarpState& st, const uint32_t (&qa)[8][4], uint32
     st.o[j][2] *= alpha[1];
     st.o[j][3] *= alpha[1];
   }
-  uint32_t pa[4];
-  pa[0] = pack_bf16(p[0][0], p[0][1]);
-  pa[1] = pack_bf16(p[0][2], p[0][3]);
-  pa[2] = pack_bf16(p[1][0], p[1][1]);
-  pa[3] = pack_bf16(p[1][2], p[1][3]);
+  // P enters the MMA as bf16 hi + lo parts (p = hi + lo to ~2^-17): a single bf16
+  // rounding of P would put ~2^-10 relative noise on the output, because the
+  // weighted sum of V rows largely cancels.
+  uint32_t pa[4], pl[4];
+  split_bf16(p[0][0], p[0][1], pa[0], pl[0]);
+  split_bf16(p[0][2], p[0][3], pa[1], pl[1]);
+  split_bf16(p[1][0], p[1][1], pa[2], pl[2]);
+  split_bf16(p[1][2], p[1][3], pa[3], pl[3]);
 
   // O += P V : B operand = V rows (token-major) via transposed ldmatrix.
 #pragma unroll
@@ -173,6 +176,8 @@ CORTEX_DEVICE void attend_tile(WarpState& st, const uint32_t (&qa)[8][4], uint32
     ldmatrix_x4_trans(kv_elem_addr(v_base, token, dim0), b00, b01, b10, b11);
     mma_bf16_16816(st.o[j], pa, b00, b01);
     mma_bf16_16816(st.o[j + 1], pa, b10, b11);
+    mma_bf16_16816(st.o[j], pl, b00, b01);
+    mma_bf16_16816(st.o[j + 1], pl, b10, b11);
   }
 }
 

@@ -219,6 +219,14 @@ CORTEX_DEVICE uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// (a, b) -> bf16x2 hi = round(a, b) and lo = round((a, b) - hi)
+CORTEX_DEVICE void split_bf16(float a, float b, uint32_t& hi, uint32_t& lo) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  const float2 hf = __bfloat1622float2(h);
+  hi = *reinterpret_cast<uint32_t*>(&h);
+  lo = pack_bf16(a - hf.x, b - hf.y);
+}
+
 CORTEX_DEVICE float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
 CORTEX_DEVICE float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
 

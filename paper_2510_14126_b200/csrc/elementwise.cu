@@ -29,14 +29,19 @@ CORTEX_DEVICE bf16x8 pack8(const float (&f)[8]) {
   return x;
 }
 
-// out[t] = emb[tok], tok = tokens[index ? index[t] : t]
+// out[t] = float(emb[tok]), tok = tokens[index ? index[t] : t]  (fp32 residual stream)
 __global__ void embed_kernel(const __nv_bfloat16* __restrict__ emb, const int* __restrict__ tokens,
-                             const int* __restrict__ index, int d, __nv_bfloat16* __restrict__ out) {
+                             const int* __restrict__ index, int d, float* __restrict__ out) {
   const int t = blockIdx.x;
   const int tok = tokens[index ? index[t] : t];
   const bf16x8* src = reinterpret_cast<const bf16x8*>(emb + static_cast<int64_t>(tok) * d);
-  bf16x8* dst = reinterpret_cast<bf16x8*>(out + static_cast<int64_t>(t) * d);
-  for (int i = threadIdx.x; i < d / 8; i += blockDim.x) dst[i] = src[i];
+  float4* dst = reinterpret_cast<float4*>(out + static_cast<int64_t>(t) * d);
+  for (int i = threadIdx.x; i < d / 8; i += blockDim.x) {
+    float f[8];
+    unpack8(src[i], f);
+    dst[2 * i] = make_float4(f[0], f[1], f[2], f[3]);
+    dst[2 * i + 1] = make_float4(f[4], f[5], f[6], f[7]);
+  }
 }
 
 CORTEX_DEVICE float block_sum(float v, float* red) {
@@ -52,13 +57,13 @@ CORTEX_DEVICE float block_sum(float v, float* red) {
 }
 
 // y[r] = bf16(x[src] * rsqrt(mean(x[src]^2) + eps) * w), src = rows ? rows[r] : r
-__global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const int* __restrict__ rows,
+__global__ void rmsnorm_kernel(const float* __restrict__ x, const int* __restrict__ rows,
                                const __nv_bfloat16* __restrict__ w, int d, float eps,
                                __nv_bfloat16* __restrict__ y) {
   __shared__ float red[32];
   const int r = blockIdx.x;
   const int src = rows ? rows[r] : r;
-  const bf16x8* xr = reinterpret_cast<const bf16x8*>(x + static_cast<int64_t>(src) * d);
+  const float4* xr = reinterpret_cast<const float4*>(x + static_cast<int64_t>(src) * d);
   const bf16x8* wr = reinterpret_cast<const bf16x8*>(w);
   bf16x8* yr = reinterpret_cast<bf16x8*>(y + static_cast<int64_t>(r) * d);
   const int nvec = d / 8;
@@ -69,7 +74,9 @@ __global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const int* _
   for (int k = 0; k < 4; ++k) {
     const int i = threadIdx.x + k * blockDim.x;
     if (i < nvec) {
-      unpack8(xr[i], f[k]);
+      const float4 a = xr[2 * i], b = xr[2 * i + 1];
+      f[k][0] = a.x; f[k][1] = a.y; f[k][2] = a.z; f[k][3] = a.w;
+      f[k][4] = b.x; f[k][5] = b.y; f[k][6] = b.z; f[k][7] = b.w;
 #pragma unroll
       for (int e = 0; e < 8; ++e) ss += f[k][e] * f[k][e];
     }
@@ -229,7 +236,7 @@ int32_t cortex_embed(const void* emb, const int32_t* tokens, const int32_t* inde
   if (!emb || !tokens || !out || n_tok < 0 || d % 8) return CORTEX_EBADARG;
   if (n_tok == 0) return CORTEX_OK;
   embed_kernel<<<n_tok, 128, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(emb), tokens,
-                                          index, d, reinterpret_cast<__nv_bfloat16*>(out));
+                                          index, d, reinterpret_cast<float*>(out));
   CORTEX_CHECK_LAUNCH();
   return CORTEX_OK;
 }
@@ -242,7 +249,7 @@ int32_t cortex_rmsnorm(const void* x, const int32_t* rows, int32_t n_rows, const
   while (threads * 8 * 4 < d) threads *= 2;
   if (threads < 64) threads = 64;
   rmsnorm_kernel<<<n_rows, threads, 0, stream>>>(
-      reinterpret_cast<const __nv_bfloat16*>(x), rows, reinterpret_cast<const __nv_bfloat16*>(w),
+      reinterpret_cast<const float*>(x), rows, reinterpret_cast<const __nv_bfloat16*>(w),
       d, eps, reinterpret_cast<__nv_bfloat16*>(y));
   CORTEX_CHECK_LAUNCH();
   return CORTEX_OK;

@@ -1,6 +1,6 @@
 // Dense projections of the stage-engine decoder on 5th-gen tensor cores.
 //
-//   C[m, n] = sum_k X[m, k] * W[n, k]        (+ residual[m, n])
+//   C[m, n] = sum_k X[m, k] * W[n, k]        (+ residual[m, n], fp32)
 //
 // X is the activation matrix [M, K] (tokens x features, bf16, row-major), W the
 // weight matrix [N, K] (nn.Linear layout, bf16). The kernel is "swap-AB": the
@@ -30,7 +30,7 @@ struct GemmArgs {
   void* out;
   int ldo;
   int out_f32;
-  const __nv_bfloat16* residual;
+  const float* residual;  // fp32 (the residual stream)
   int ldr;
   int kb_per_split;
   int splits;
@@ -56,7 +56,7 @@ CORTEX_DEVICE void store_cols(const GemmArgs& a, int n, int m_base, const float 
     const int m = m_base + j;
     if (m < a.M) {
       float x = v[j];
-      if (a.residual) x += __bfloat162float(a.residual[static_cast<size_t>(m) * a.ldr + n]);
+      if (a.residual) x += a.residual[static_cast<size_t>(m) * a.ldr + n];
       if (a.out_f32) {
         reinterpret_cast<float*>(a.out)[static_cast<size_t>(m) * a.ldo + n] = x;
       } else {
@@ -313,7 +313,7 @@ int32_t cortex_gemm_bf16(const void* tmap_w, const void* tmap_x, int32_t M, int3
   a.out = out;
   a.ldo = ldo;
   a.out_f32 = out_f32;
-  a.residual = reinterpret_cast<const __nv_bfloat16*>(residual);
+  a.residual = reinterpret_cast<const float*>(residual);
   a.ldr = ldr;
   const int total_kb = K / kBlockK;
   const int splits = cortex_gemm_splits(M, N, K);

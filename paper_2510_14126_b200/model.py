@@ -1,0 +1,358 @@
+"""Decoder forward of a stage engine on one B200.
+
+`GpuWorker` owns everything device-resident on one GPU: the random-init bf16
+weights (one model serves every stage), the paged KV arena
+(cache, block table, per-row generated-token state) shared by the engines placed
+on this GPU (each engine owns disjoint block ids and table rows), and the
+activation buffers. `forward(plan)` runs one batched step over a mix of decode
+tokens (one per call, attention via the split-K decode kernel) and prefill
+tokens (prompts / stage prefixes, causal paged prefill kernel): one weight
+stream per step, every projection a tcgen05 GEMM.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import ops
+from .config import BLOCK_TOKENS, HEAD_DIM, ModelConfig
+
+BF16 = torch.bfloat16
+
+
+def rope_tables(max_pos: int, theta: float) -> tuple[np.ndarray, np.ndarray]:
+    """cos/sin [max_pos, 64] fp32, angle = pos * theta^(-2i/128) evaluated in float64."""
+    inv = theta ** (-np.arange(0, HEAD_DIM, 2, dtype=np.float64) / HEAD_DIM)
+    ang = np.arange(max_pos, dtype=np.float64)[:, None] * inv[None, :]
+    return np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32)
+
+
+def init_weights(cfg: ModelConfig, device, seed: int = 0, std: float = 0.02) -> dict:
+    """Random-init weights, N(0, std^2) projections, norms 1 + N(0, 0.1^2)."""
+    g = torch.Generator(device=device).manual_seed(seed)
+
+    def rnd(*shape, s=std):
+        return (torch.randn(*shape, generator=g, device=device) * s).to(BF16)
+
+    def norm(d):
+        return (1.0 + 0.1 * torch.randn(d, generator=g, device=device)).to(BF16)
+
+    d = cfg.d_model
+    w = {"embed": rnd(cfg.vocab, d, s=1.0)}
+    for i in range(cfg.n_layers):
+        p = f"layers.{i}."
+        w[p + "attn_norm"] = norm(d)
+        w[p + "wqkv"] = rnd(cfg.qkv_dim, d)
+        w[p + "wo"] = rnd(d, cfg.n_heads * HEAD_DIM)
+        w[p + "mlp_norm"] = norm(d)
+        w[p + "wgu"] = rnd(2 * cfg.ffn, d)
+        w[p + "wd"] = rnd(d, cfg.ffn)
+    w["final_norm"] = norm(d)
+    w["lm_head"] = rnd(cfg.vocab, d)
+    return w
+
+
+@dataclass
+class PrefillSeq:
+    """New tokens of one sequence: positions [kv_len - n, kv_len) of table row `row`."""
+
+    row: int
+    prefix_len: int  # tokens of the row's prefix segment (0 when prefilling a prefix row)
+    kv_len: int      # total tokens of the sequence after this step
+    tokens: np.ndarray
+    out_row: int = -1   # table row receiving the greedy token of the last position (-1: none)
+    hist_pos: int = 0
+
+
+@dataclass
+class DecodeTok:
+    """One decode token of row `row` at position kv_len - 1 (input = slot_tok[row])."""
+
+    row: int
+    prefix_len: int
+    kv_len: int
+    hist_pos: int
+
+
+def token_slot(prefix_len: int, pos: int) -> tuple[int, int]:
+    """(block column, offset) of logical position `pos` in a row with a prefix segment."""
+    if pos < prefix_len:
+        return pos // BLOCK_TOKENS, pos % BLOCK_TOKENS
+    npb = (prefix_len + BLOCK_TOKENS - 1) // BLOCK_TOKENS
+    j = pos - prefix_len
+    return npb + j // BLOCK_TOKENS, j % BLOCK_TOKENS
+
+
+@dataclass
+class StepPlan:
+    decode: list[DecodeTok] = field(default_factory=list)
+    prefill: list[PrefillSeq] = field(default_factory=list)
+
+    @property
+    def n_tokens(self) -> int:
+        return len(self.decode) + sum(len(p.tokens) for p in self.prefill)
+
+
+class GpuWorker:
+    """Weights + KV arena + activation buffers of one GPU."""
+
+    def __init__(self, cfg: ModelConfig, device, n_blocks: int, n_rows: int, row_cols: int,
+                 max_tokens: int = 4096, max_out: int = 512, hist_cols: int = 1024,
+                 max_seq_tokens: int = 16384, weights: dict | None = None, seed: int = 0) -> None:
+        self.cfg = cfg
+        self.device = torch.device(device)
+        self.n_blocks = n_blocks
+        self.max_tokens = max_tokens
+        self.max_out = max_out
+        self.max_seq_tokens = max_seq_tokens
+        dev = self.device
+        self.w = weights if weights is not None else init_weights(cfg, dev, seed)
+        self.wmap = {k: ops.weight_map(v) for k, v in self.w.items() if v.dim() == 2 and k != "embed"}
+        cos, sin = rope_tables(max_seq_tokens + 1, cfg.rope_theta)
+        self.cos = torch.from_numpy(cos).to(dev)
+        self.sin = torch.from_numpy(sin).to(dev)
+        # paged KV arena
+        self.cache = torch.empty(cfg.n_layers, 2, n_blocks, cfg.n_kv_heads, BLOCK_TOKENS, HEAD_DIM,
+                                 dtype=BF16, device=dev)
+        self.kvmap = ops.kv_map(self.cache.view(-1, HEAD_DIM))
+        self.table = torch.zeros(n_rows, row_cols, dtype=torch.int32, device=dev)
+        self.slot_tok = torch.zeros(n_rows, dtype=torch.int32, device=dev)
+        self.hist = torch.zeros(n_rows, hist_cols, dtype=torch.int32, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        # activations
+        d, T = cfg.d_model, max_tokens
+        self.x = torch.zeros(T, d, dtype=torch.float32, device=dev)  # fp32 residual stream
+        self.xn = torch.zeros(T, d, dtype=BF16, device=dev)
+        self.qkv = torch.zeros(T, cfg.qkv_dim, dtype=BF16, device=dev)
+        self.q = torch.zeros(T, cfg.n_heads * HEAD_DIM, dtype=BF16, device=dev)
+        self.attn = torch.zeros(T, cfg.n_heads * HEAD_DIM, dtype=BF16, device=dev)
+        self.gu = torch.zeros(T, 2 * cfg.ffn, dtype=BF16, device=dev)
+        self.act = torch.zeros(T, cfg.ffn, dtype=BF16, device=dev)
+        self.xn_out = torch.zeros(max_out, d, dtype=BF16, device=dev)
+        self.logits = torch.zeros(max_out, cfg.vocab, dtype=torch.float32, device=dev)
+        self.out_tok = torch.zeros(max_out, dtype=torch.int32, device=dev)
+        self.xn_map = ops.act_map(self.xn)
+        self.attn_map = ops.act_map(self.attn)
+        self.act_map = ops.act_map(self.act)
+        self.xn_out_map = ops.act_map(self.xn_out)
+        self.gemm_ws = ops.GemmWorkspace(dev)
+        self.max_splits = ops.decode_splits(0, max_seq_tokens) + 1
+        self.o_part = torch.empty(max_out * self.max_splits * cfg.n_heads * HEAD_DIM,
+                                  dtype=torch.float32, device=dev)
+        self.lse_part = torch.empty(max_out * self.max_splits * cfg.n_heads, dtype=torch.float32,
+                                    device=dev)
+        # metadata staging (one H2D copy per step)
+        self._meta_cap = 16 * (T + max_out) + 64
+        self._ring = 8  # pinned staging buffers, reused only after their copy ran
+        self.meta_dev_small = torch.zeros(4 * 4096, dtype=torch.int32, device=dev)
+        self.h2d_bytes = 0
+        self.meta_host = [torch.zeros(self._meta_cap, dtype=torch.int32, pin_memory=True)
+                          for _ in range(self._ring)]
+        self.meta_evt = [None] * self._ring
+        self._meta_i = 0
+        self.meta_dev = torch.zeros(self._meta_cap, dtype=torch.int32, device=dev)
+        self.scale = 1.0 / math.sqrt(HEAD_DIM)
+        self.launches = 0  # kernels of this library launched since construction
+        self.steps = 0
+        self.on_forward = None  # optional hook(plan, n_out) for parity checking
+
+    # ------------------------------------------------------------------ helpers
+
+    def layer_rows(self, layer: int) -> tuple[int, int]:
+        per_plane = self.n_blocks * self.cfg.n_kv_heads * BLOCK_TOKENS
+        return (2 * layer) * per_plane, (2 * layer + 1) * per_plane
+
+    def _upload(self, arrays: list[np.ndarray], dev_buf: torch.Tensor | None = None
+                ) -> list[torch.Tensor]:
+        """Stage int32 arrays through a pinned ring into `dev_buf` (one async H2D copy).
+        A device buffer may be rewritten by the next upload: stream order guarantees
+        the kernels that read it ran first."""
+        dev_buf = self.meta_dev if dev_buf is None else dev_buf
+        sizes = [a.size for a in arrays]
+        total = sum(sizes)
+        if total > min(self._meta_cap, dev_buf.numel()):
+            raise ValueError("step metadata exceeds staging capacity")
+        i = self._meta_i
+        self._meta_i = (i + 1) % self._ring
+        if self.meta_evt[i] is not None:
+            self.meta_evt[i].synchronize()
+        buf = self.meta_host[i]
+        host = buf.numpy()
+        off = 0
+        offs = []
+        for a in arrays:
+            host[off:off + a.size] = a
+            offs.append(off)
+            off += a.size
+        dev_buf[:total].copy_(buf[:total], non_blocking=True)
+        evt = torch.cuda.Event()
+        evt.record()
+        self.meta_evt[i] = evt
+        self.h2d_bytes += 4 * total
+        return [dev_buf[o:o + n] for o, n in zip(offs, sizes)]
+
+    def upload_small(self, arrays: list[np.ndarray]) -> list[torch.Tensor]:
+        """Staging for allocator / table requests (separate device buffer)."""
+        return self._upload(arrays, self.meta_dev_small)
+
+    def alloc_blocks(self, pool, reqs: list[tuple[int, int, int]]) -> None:
+        """Allocate from `pool` (an EngineSlice): reqs = (table row, first col, blocks)."""
+        counts, rows, cols = self.upload_small([
+            np.asarray([r[2] for r in reqs], np.int32), np.asarray([r[0] for r in reqs], np.int32),
+            np.asarray([r[1] for r in reqs], np.int32)])
+        ops.kv_alloc(pool.bitmap, pool.n_blocks, pool.block_base, counts, rows, cols, len(reqs),
+                     self.table, self.status)
+        self.launches += 1
+
+    def free_blocks(self, pool, reqs: list[tuple[int, int, int]]) -> None:
+        rows, cols, counts = self.upload_small([
+            np.asarray([r[0] for r in reqs], np.int32), np.asarray([r[1] for r in reqs], np.int32),
+            np.asarray([r[2] for r in reqs], np.int32)])
+        ops.kv_free(pool.bitmap, pool.n_blocks, pool.block_base, self.table, rows, cols, counts,
+                    len(reqs), self.status)
+        self.launches += 1
+
+    def copy_prefix_row(self, src_row: int, dst_row: int, n_blocks: int) -> None:
+        src, dst, col, cnt = self.upload_small([np.asarray([v], np.int32)
+                                                for v in (src_row, dst_row, 0, n_blocks)])
+        ops.table_copy(self.table, src, dst, col, cnt, 1)
+        self.launches += 1
+
+    def copy_first_token(self, src_row: int, dst_row: int) -> None:
+        """Empty-prompt call on a resident prefix: its first token is the prefix's."""
+        self.slot_tok[dst_row] = self.slot_tok[src_row]
+        self.hist[dst_row, 0] = self.slot_tok[src_row]
+
+    def forward_prefill_chunk(self, seq: PrefillSeq) -> int:
+        return self.forward(StepPlan(prefill=[seq]))
+
+    def forward_decode(self, toks: list[DecodeTok]) -> int:
+        return self.forward(StepPlan(decode=toks))
+
+    # ------------------------------------------------------------------ forward
+
+    @torch.no_grad()
+    def forward(self, plan: StepPlan) -> int:
+        """Run one batched step; returns the number of greedy tokens produced."""
+        cfg = self.cfg
+        n_dec = len(plan.decode)
+        T = plan.n_tokens
+        if T == 0:
+            return 0
+        if T > self.max_tokens:
+            raise ValueError(f"step of {T} tokens exceeds max_tokens={self.max_tokens}")
+        i32 = np.int32
+        pos = np.empty(T, i32)
+        app_col = np.empty(T, i32)
+        app_off = np.empty(T, i32)
+        app_row = np.empty(T, i32)
+        tok_ids = np.zeros(T, i32)
+        dec_row = np.empty(n_dec, i32)
+        dec_prefix = np.empty(n_dec, i32)
+        dec_kvlen = np.empty(n_dec, i32)
+        out_rows, out_slot, out_hist = [], [], []
+        for i, d in enumerate(plan.decode):
+            p = d.kv_len - 1
+            c, o = token_slot(d.prefix_len, p)
+            pos[i], app_row[i], app_col[i], app_off[i] = p, d.row, c, o
+            dec_row[i], dec_prefix[i], dec_kvlen[i] = d.row, d.prefix_len, d.kv_len
+            out_rows.append(i)
+            out_slot.append(d.row)
+            out_hist.append(d.hist_pos)
+        n_pf = len(plan.prefill)
+        pf_row = np.empty(n_pf, i32)
+        pf_prefix = np.empty(n_pf, i32)
+        pf_kvlen = np.empty(n_pf, i32)
+        pf_qstart = np.empty(n_pf, i32)
+        pf_qlen = np.empty(n_pf, i32)
+        t = n_dec
+        max_qlen = 0
+        for j, s in enumerate(plan.prefill):
+            n = len(s.tokens)
+            p0 = s.kv_len - n
+            ps = np.arange(p0, s.kv_len, dtype=np.int64)
+            pos[t:t + n] = ps
+            app_row[t:t + n] = s.row
+            if s.prefix_len == 0:
+                app_col[t:t + n] = ps // BLOCK_TOKENS
+                app_off[t:t + n] = ps % BLOCK_TOKENS
+            else:
+                npb = (s.prefix_len + BLOCK_TOKENS - 1) // BLOCK_TOKENS
+                jj = ps - s.prefix_len
+                if (jj < 0).any():
+                    raise ValueError("prefill of a private segment cannot write prefix positions")
+                app_col[t:t + n] = npb + jj // BLOCK_TOKENS
+                app_off[t:t + n] = jj % BLOCK_TOKENS
+            tok_ids[t:t + n] = s.tokens
+            pf_row[j], pf_prefix[j], pf_kvlen[j], pf_qstart[j], pf_qlen[j] = (
+                s.row, s.prefix_len, s.kv_len, t, n)
+            max_qlen = max(max_qlen, n)
+            if s.out_row >= 0:
+                out_rows.append(t + n - 1)
+                out_slot.append(s.out_row)
+                out_hist.append(s.hist_pos)
+            t += n
+        n_out = len(out_rows)
+        if n_out > self.max_out:
+            raise ValueError("too many output rows in one step")
+        (d_pos, d_arow, d_acol, d_aoff, d_tok, d_drow, d_dpre, d_dkv, d_prow, d_ppre, d_pkv,
+         d_pqs, d_pql, d_orow, d_oslot, d_ohist) = self._upload([
+            pos, app_row, app_col, app_off, tok_ids, dec_row, dec_prefix, dec_kvlen, pf_row,
+            pf_prefix, pf_kvlen, pf_qstart, pf_qlen, np.asarray(out_rows, i32),
+            np.asarray(out_slot, i32), np.asarray(out_hist, i32)])
+        max_splits = 1
+        if n_dec:
+            max_splits = max(ops.decode_splits(int(a), int(b)) for a, b in zip(dec_prefix, dec_kvlen))
+            if max_splits > self.max_splits:
+                raise ValueError("decode context exceeds max_seq_tokens")
+        w, wm = self.w, self.wmap
+        x, xn, ws = self.x, self.xn, self.gemm_ws
+        hq, hkv = cfg.n_heads, cfg.n_kv_heads
+        nl = 0
+        if n_dec:
+            ops.embed(w["embed"], self.slot_tok, n_dec, x, index=d_drow)
+            nl += 1
+        if T > n_dec:
+            ops.embed(w["embed"], d_tok[n_dec:], T - n_dec, x[n_dec:])
+            nl += 1
+        o_part = self.o_part[: max(n_dec, 1) * max_splits * hq * HEAD_DIM]
+        lse_part = self.lse_part[: max(n_dec, 1) * max_splits * hq]
+        for li in range(cfg.n_layers):
+            p = f"layers.{li}."
+            k0, v0 = self.layer_rows(li)
+            ops.rmsnorm(x, w[p + "attn_norm"], T, xn, cfg.eps)
+            ops.gemm(wm[p + "wqkv"], self.xn_map, T, self.qkv, ws)
+            ops.rope_kv_append(self.qkv, self.q, self.cache, k0, v0, self.table, d_pos, d_arow,
+                               d_acol, d_aoff, self.cos, self.sin, T, hq, hkv)
+            nl += 3
+            if n_dec:
+                ops.paged_decode_attn(self.kvmap, self.q, self.table, d_drow, d_dpre, d_dkv, n_dec,
+                                      hkv, cfg.group, k0, v0, self.scale, o_part, lse_part,
+                                      max_splits, self.attn)
+                nl += 2
+            if n_pf:
+                ops.paged_prefill_attn(self.kvmap, self.q, self.attn, self.table, d_prow, d_ppre,
+                                       d_pkv, d_pqs, d_pql, n_pf, max_qlen, hkv, cfg.group, k0, v0,
+                                       self.scale)
+                nl += 1
+            ops.gemm(wm[p + "wo"], self.attn_map, T, x, ws, residual=x)
+            ops.rmsnorm(x, w[p + "mlp_norm"], T, xn, cfg.eps)
+            ops.gemm(wm[p + "wgu"], self.xn_map, T, self.gu, ws)
+            ops.swiglu(self.gu, T, self.act)
+            ops.gemm(wm[p + "wd"], self.act_map, T, x, ws, residual=x)
+            nl += 5
+        if n_out:
+            ops.rmsnorm(x, w["final_norm"], n_out, self.xn_out, cfg.eps, rows=d_orow)
+            ops.gemm(wm["lm_head"], self.xn_out_map, n_out, self.logits, ws)
+            ops.argmax(self.logits, n_out, cfg.vocab, out_tok=self.out_tok, slot=d_oslot,
+                       slot_tok=self.slot_tok, hist=self.hist, hist_pos=d_ohist)
+            nl += 3
+        self.launches += nl
+        self.steps += 1
+        if self.on_forward is not None:
+            self.on_forward(plan, n_out)
+        return n_out

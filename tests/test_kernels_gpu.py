@@ -62,12 +62,14 @@ def test_gemm_residual_and_f32(cuda, M):
     g = torch.Generator(device=cuda).manual_seed(7 + M)
     x = torch.randn(max(M, 32), K, generator=g, device=cuda).to(torch.bfloat16)
     w = (torch.randn(N, K, generator=g, device=cuda) * 0.05).to(torch.bfloat16)
-    r = torch.randn(M, N, generator=g, device=cuda).to(torch.bfloat16)
+    r = torch.randn(M, N, generator=g, device=cuda)
     ws = o.GemmWorkspace(cuda)
-    out = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    out = torch.empty(M, N, device=cuda, dtype=torch.float32)
     o.gemm(o.weight_map(w), o.act_map(x), M, out, ws, residual=r)
-    ref = x[:M].float() @ w.float().T + r.float()
-    assert rel(out, ref) < 4e-3
+    ref = x[:M].float() @ w.float().T + r
+    assert rel(out, ref) < 1e-5
+    o.gemm(o.weight_map(w), o.act_map(x), M, r, ws, residual=r)  # in place (residual stream)
+    assert rel(r, ref) < 1e-5
     out32 = torch.empty(M, N, device=cuda, dtype=torch.float32)
     o.gemm(o.weight_map(w), o.act_map(x), M, out32, ws)
     assert rel(out32, x[:M].float() @ w.float().T) < 1e-5
@@ -210,9 +212,9 @@ def test_rmsnorm_embed_swiglu_argmax(cuda):
     g = torch.Generator(device=cuda).manual_seed(1)
     emb = torch.randn(V, d, generator=g, device=cuda).to(torch.bfloat16)
     toks = torch.randint(0, V, (T,), generator=g, device=cuda, dtype=torch.int32)
-    h = torch.empty(T, d, device=cuda, dtype=torch.bfloat16)
+    h = torch.empty(T, d, device=cuda, dtype=torch.float32)
     o.embed(emb, toks, T, h)
-    assert torch.equal(h, emb[toks.long()])
+    assert torch.equal(h, emb[toks.long()].float())
     w = (1 + 0.1 * torch.randn(d, generator=g, device=cuda)).to(torch.bfloat16)
     y = torch.empty(T, d, device=cuda, dtype=torch.bfloat16)
     o.rmsnorm(h, w, T, y, 1e-5)
