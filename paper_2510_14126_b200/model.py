@@ -76,6 +76,42 @@ class DecodeTok:
     prefix_len: int
     kv_len: int
     hist_pos: int
+    prefix_key: int = -1  # identity of the shared prefix segment (unique-bytes accounting)
+
+
+class KernelProfile:
+    """CUDA-event timing of selected kernel classes inside forward() (bench only).
+
+    Each record: (class, start event, end event, algorithmic bytes, flops)."""
+
+    def __init__(self, classes) -> None:
+        self.classes = set(classes)
+        self.recs: list = []
+
+    def open(self, cls):
+        if cls not in self.classes:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    def close(self, cls, e0, nbytes: float, flops: float) -> None:
+        if e0 is None:
+            return
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        self.recs.append((cls, e0, e1, nbytes, flops))
+
+    def summary(self) -> dict:
+        torch.cuda.synchronize()
+        out: dict = {}
+        for cls, e0, e1, b, f in self.recs:
+            d = out.setdefault(cls, {"launches": 0, "ms": 0.0, "bytes": 0.0, "flops": 0.0})
+            d["launches"] += 1
+            d["ms"] += e0.elapsed_time(e1)
+            d["bytes"] += b
+            d["flops"] += f
+        return out
 
 
 def token_slot(prefix_len: int, pos: int) -> tuple[int, int]:
@@ -159,6 +195,7 @@ class GpuWorker:
         self.launches = 0  # kernels of this library launched since construction
         self.steps = 0
         self.on_forward = None  # optional hook(plan, n_out) for parity checking
+        self.prof: KernelProfile | None = None  # optional per-kernel-class CUDA-event timing
 
     # ------------------------------------------------------------------ helpers
 
@@ -321,33 +358,60 @@ class GpuWorker:
             nl += 1
         o_part = self.o_part[: max(n_dec, 1) * max_splits * hq * HEAD_DIM]
         lse_part = self.lse_part[: max(n_dec, 1) * max_splits * hq]
+        prof = self.prof
+        tok_kv_bytes = hkv * HEAD_DIM * 2 * 2  # K + V of one token in one layer
+        if prof is not None:
+            uniq = sum(d.kv_len - d.prefix_len for d in plan.decode)
+            uniq += sum({(d.prefix_key if d.prefix_key >= 0 else ("row", d.row)): d.prefix_len
+                         for d in plan.decode}.values())
+            dec_bytes = uniq * tok_kv_bytes + n_dec * hq * HEAD_DIM * 2 * 2
+            dec_flops = 4.0 * hq * HEAD_DIM * float(dec_kvlen.sum())
+            pf_keys = sum(int(q) * (int(k) - int(q)) + int(q) * (int(q) + 1) // 2
+                          for q, k in zip(pf_qlen, pf_kvlen))
+            pf_bytes = float(pf_kvlen.sum()) * tok_kv_bytes + 2 * 2 * (T - n_dec) * hq * HEAD_DIM
+            pf_flops = 4.0 * hq * HEAD_DIM * pf_keys
+
+        def gemm(name, xmap, M, out, residual=None):
+            e0 = prof.open("gemm") if prof is not None else None
+            ops.gemm(wm[name], xmap, M, out, ws, residual=residual)
+            if e0 is not None:
+                N, K = wm[name].rows, wm[name].cols
+                ob = out.element_size() * (2 if residual is not None else 1)
+                prof.close("gemm", e0, 2.0 * N * K + 2.0 * M * K + ob * M * N, 2.0 * M * N * K)
+
         for li in range(cfg.n_layers):
             p = f"layers.{li}."
             k0, v0 = self.layer_rows(li)
             ops.rmsnorm(x, w[p + "attn_norm"], T, xn, cfg.eps)
-            ops.gemm(wm[p + "wqkv"], self.xn_map, T, self.qkv, ws)
+            gemm(p + "wqkv", self.xn_map, T, self.qkv)
             ops.rope_kv_append(self.qkv, self.q, self.cache, k0, v0, self.table, d_pos, d_arow,
                                d_acol, d_aoff, self.cos, self.sin, T, hq, hkv)
             nl += 3
             if n_dec:
+                e0 = prof.open("attn_decode") if prof is not None else None
                 ops.paged_decode_attn(self.kvmap, self.q, self.table, d_drow, d_dpre, d_dkv, n_dec,
                                       hkv, cfg.group, k0, v0, self.scale, o_part, lse_part,
                                       max_splits, self.attn)
+                if e0 is not None:
+                    prof.close("attn_decode", e0, dec_bytes, dec_flops)
                 nl += 2
             if n_pf:
+                e0 = prof.open("attn_prefill") if prof is not None else None
                 ops.paged_prefill_attn(self.kvmap, self.q, self.attn, self.table, d_prow, d_ppre,
                                        d_pkv, d_pqs, d_pql, n_pf, max_qlen, hkv, cfg.group, k0, v0,
                                        self.scale)
+                if e0 is not None:
+                    prof.close("attn_prefill", e0, pf_bytes, pf_flops)
                 nl += 1
-            ops.gemm(wm[p + "wo"], self.attn_map, T, x, ws, residual=x)
+            gemm(p + "wo", self.attn_map, T, x, residual=x)
             ops.rmsnorm(x, w[p + "mlp_norm"], T, xn, cfg.eps)
-            ops.gemm(wm[p + "wgu"], self.xn_map, T, self.gu, ws)
+            gemm(p + "wgu", self.xn_map, T, self.gu)
             ops.swiglu(self.gu, T, self.act)
-            ops.gemm(wm[p + "wd"], self.act_map, T, x, ws, residual=x)
+            gemm(p + "wd", self.act_map, T, x, residual=x)
             nl += 5
         if n_out:
             ops.rmsnorm(x, w["final_norm"], n_out, self.xn_out, cfg.eps, rows=d_orow)
-            ops.gemm(wm["lm_head"], self.xn_out_map, n_out, self.logits, ws)
+            gemm("lm_head", self.xn_out_map, n_out, self.logits)
             ops.argmax(self.logits, n_out, cfg.vocab, out_tok=self.out_tok, slot=d_oslot,
                        slot_tok=self.slot_tok, hist=self.hist, hist_pos=d_ohist)
             nl += 3
