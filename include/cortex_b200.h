@@ -94,6 +94,11 @@ int32_t cortex_tmap_encode_2d_bf16(void* tmap_out, const void* gptr, uint64_t ro
  * tmap_w over W [N, K] with box (128, 64); tmap_x over X [>= M, K] with box (32, 64).
  * workspace / counters are used when cortex_gemm_splits(M, N, K) > 1. */
 int32_t cortex_gemm_splits(int32_t M, int32_t N, int32_t K);
+/* Which kernel serves (M, N, K): 1 = 1-SM swap-AB + split-K (decode sizes),
+ * 2 = persistent 2-SM cta_group::2 kernel (M > 128, N % 256 == 0). */
+int32_t cortex_gemm_path(int32_t M, int32_t N, int32_t K);
+/* Test hook: 0 = automatic, 1 = force the 1-SM kernel, 2 = force 2-SM when legal. */
+int32_t cortex_gemm_set_mode(int32_t mode);
 int32_t cortex_gemm_bf16(const void* tmap_w, const void* tmap_x, int32_t M, int32_t N, int32_t K,
                          void* out, int32_t ldo, int32_t out_f32, const void* residual,
                          int32_t ldr, float* workspace, uint64_t workspace_bytes,
@@ -126,8 +131,14 @@ int32_t cortex_argmax(const float* logits, int64_t ld, int32_t n_rows, int32_t v
 
 /* Paged decode attention (one query token per sequence), split along the
  * context in fixed 256-token chunks + LSE combine. o_part/lse_part:
- * [n_seqs, max_splits, Hq, 128] / [n_seqs, max_splits, Hq] fp32 workspace,
- * max_splits >= max over seqs of cortex_decode_splits(prefix, kv_len). */
+ * [n_seqs, max_splits, Hq, 128] / [n_seqs, max_splits, Hq] fp32 workspace.
+ * Without groups (n_groups = 0): max_splits >= max cortex_decode_splits(prefix, kv_len).
+ * Cascade (n_groups > 0): the decode calls sharing a resident stage prefix are
+ * contiguous (group g = calls [grp_first, grp_first + grp_count), prefix in table row
+ * grp_row, grp_plen tokens); their prefix attention runs once per group (partials in
+ * slots [0, prefix_slots), prefix_slots >= max ceil(ceil(P/16)/16)), the private
+ * tokens per call (slots prefix_slots + ...). Every call with prefix_len > 0 must
+ * belong to a group. max_group_count = largest grp_count. */
 int32_t cortex_decode_splits(int32_t prefix_len, int32_t kv_len);
 int32_t cortex_paged_decode_attn(const void* tmap_kv, const void* q, const int32_t* table,
                                  int32_t table_stride, const int32_t* seq_row,
@@ -135,7 +146,10 @@ int32_t cortex_paged_decode_attn(const void* tmap_kv, const void* q, const int32
                                  int32_t n_seqs, int32_t n_kv_heads, int32_t group,
                                  int64_t k_row0, int64_t v_row0, float softmax_scale,
                                  float* o_part, float* lse_part, int32_t max_splits, void* out,
-                                 cortex_stream_t stream);
+                                 const int32_t* grp_row, const int32_t* grp_plen,
+                                 const int32_t* grp_first, const int32_t* grp_count,
+                                 int32_t n_groups, int32_t max_group_count,
+                                 int32_t prefix_slots, cortex_stream_t stream);
 
 /* Paged prefill attention: the last seq_qlen[s] positions of each sequence
  * attend causally to its prefix + private tokens. */

@@ -27,6 +27,8 @@ SIGNATURES: dict[str, list] = {
     "cortex_kv_count_free": [P, I32, P, P],
     "cortex_tmap_encode_2d_bf16": [P, P, U64, U64, U64, ctypes.c_uint32, ctypes.c_uint32],
     "cortex_gemm_splits": [I32, I32, I32],
+    "cortex_gemm_path": [I32, I32, I32],
+    "cortex_gemm_set_mode": [I32],
     "cortex_gemm_bf16": [P, P, I32, I32, I32, P, I32, I32, P, I32, P, U64, P, I32, P],
     "cortex_embed": [P, P, P, I32, I32, P, P],
     "cortex_rmsnorm": [P, P, I32, P, I32, F32, P, P],
@@ -35,7 +37,7 @@ SIGNATURES: dict[str, list] = {
     "cortex_argmax": [P, I64, I32, I32, P, P, P, P, I32, P, P],
     "cortex_decode_splits": [I32, I32],
     "cortex_paged_decode_attn": [P, P, P, I32, P, P, P, I32, I32, I32, I64, I64, F32, P, P, I32,
-                                 P, P],
+                                 P, P, P, P, P, I32, I32, I32, P],
     "cortex_paged_prefill_attn": [P, P, P, P, I32, P, P, P, P, P, I32, I32, I32, I32, I64, I64,
                                   F32, P],
 }

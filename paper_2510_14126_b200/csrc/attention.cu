@@ -232,10 +232,13 @@ struct DecodeArgs {
   float scale_log2;
   float* o_part;    // [B, max_splits, Hq, 128]
   float* lse_part;  // [B, max_splits, Hq]
-  int max_splits;
+  int max_splits;   // slots per sequence
+  int cascade;      // 1: prefix tiles are handled by the shared-prefix kernel
+  int slot_off;     // first slot of the private splits (cascade only)
 };
 
 constexpr int kDecodeStages = 2;
+constexpr int kPrefillStages = 3;
 
 __global__ void __launch_bounds__(kWarps * 32)
     paged_decode_kernel(const __grid_constant__ CUtensorMap tmap_kv, const DecodeArgs a) {
@@ -249,7 +252,8 @@ __global__ void __launch_bounds__(kWarps * 32)
   const int prefix = __ldg(&a.seq_prefix[b]);
   const int kvlen = __ldg(&a.seq_kvlen[b]);
   const int ntiles = num_tiles(prefix, kvlen);
-  const int t_begin = split * kTilesPerSplit;
+  const int first_tile = a.cascade ? (prefix + kTile - 1) / kTile : 0;
+  const int t_begin = first_tile + split * kTilesPerSplit;
   if (t_begin >= ntiles) return;
   const int t_end = min(ntiles, t_begin + kTilesPerSplit);
   const int warp = warp_id();
@@ -330,9 +334,127 @@ __global__ void __launch_bounds__(kWarps * 32)
       O += co[(w * 8 + r) * kHeadDim + d] * f;
     }
     const int h = kvh * a.group + r;
-    const int64_t pidx = (static_cast<int64_t>(b) * a.max_splits + split) * hq + h;
+    const int64_t pidx =
+        (static_cast<int64_t>(b) * a.max_splits + (a.cascade ? a.slot_off : 0) + split) * hq + h;
     a.o_part[pidx * kHeadDim + d] = O / L;
     if (d == 0) a.lse_part[pidx] = M + log2f(L);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// shared-prefix ("cascade") decode attention: every decode query of the calls that
+// share one resident stage prefix attends to that prefix in one pass, so the
+// prefix's KV is read once per step instead of once per call. Grid
+// (query chunk, kv_head, group * max_psplits); each warp owns 16/group calls x
+// group heads; prefix tiles are split in 16-tile chunks (partials -> slots 0..).
+
+struct CascadeArgs {
+  const __nv_bfloat16* q;  // [B, Hq, 128] decode queries, groups contiguous
+  const int* table;
+  int table_stride;
+  const int* grp_row;    // prefix's table row
+  const int* grp_plen;   // prefix tokens
+  const int* grp_first;  // first decode index of the group
+  const int* grp_count;  // decode calls in the group
+  int max_psplits;
+  int n_kv_heads;
+  int group;
+  int64_t k_row0, v_row0;
+  float scale_log2;
+  float* o_part;
+  float* lse_part;
+  int max_splits;  // slots per sequence
+};
+
+__global__ void __launch_bounds__(kWarps * 32)
+    cascade_prefix_kernel(const __grid_constant__ CUtensorMap tmap_kv, const CascadeArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  const int chunk = blockIdx.x;
+  const int kvh = blockIdx.y;
+  const int gi = blockIdx.z / a.max_psplits;
+  const int ps = blockIdx.z % a.max_psplits;
+  const int seqs_per_warp = 16 / a.group;
+  const int seqs_per_cta = seqs_per_warp * kWarps;
+  const int count = __ldg(&a.grp_count[gi]);
+  const int s0 = chunk * seqs_per_cta;
+  if (s0 >= count) return;
+  const int plen = __ldg(&a.grp_plen[gi]);
+  const int npb = (plen + kTile - 1) / kTile;
+  const int t_begin = ps * kTilesPerSplit;
+  if (t_begin >= npb) return;
+  const int t_end = min(npb, t_begin + kTilesPerSplit);
+  const int ntl = t_end - t_begin;
+  const int first = __ldg(&a.grp_first[gi]);
+  const int row = __ldg(&a.grp_row[gi]);
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int hq = a.n_kv_heads * a.group;
+
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPrefillStages * kStageBytes);
+  uint64_t* empty = full + kPrefillStages;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kPrefillStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int* table_row = a.table + static_cast<int64_t>(row) * a.table_stride;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < min(ntl, kPrefillStages); ++i) {
+      const TileRef t = tile_ref(table_row, plen, plen, t_begin + i);
+      load_tile(smem + i * kStageBytes, &tmap_kv, &full[i], a.k_row0, a.v_row0, t.block, kvh,
+                a.n_kv_heads);
+    }
+  }
+  const int ws0 = s0 + warp * seqs_per_warp;  // first call (within group) of this warp
+  const int wn = max(0, min(seqs_per_warp, count - ws0));
+  uint32_t qa[8][4];
+  load_q_frags(qa, a.q, static_cast<int64_t>(first) + ws0, static_cast<int64_t>(hq) * kHeadDim,
+               kvh * a.group, a.group, wn * a.group);
+  WarpState st;
+  state_init(st);
+  const int qpos[2] = {0x7fffffff, 0x7fffffff};  // decode queries follow the whole prefix
+  for (int i = 0; i < ntl; ++i) {
+    const int sidx = i % kPrefillStages;
+    const TileRef t = tile_ref(table_row, plen, plen, t_begin + i);
+    mbar_wait(&full[sidx], (i / kPrefillStages) & 1);
+    if (wn > 0) attend_tile(st, qa, smem_u32(smem + sidx * kStageBytes), t, qpos, a.scale_log2);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[sidx]);
+    const int nxt = i + kPrefillStages;
+    if (threadIdx.x == 0 && nxt < ntl) {
+      mbar_wait(&empty[sidx], (i / kPrefillStages) & 1);
+      fence_proxy_async();
+      const TileRef tn = tile_ref(table_row, plen, plen, t_begin + nxt);
+      load_tile(smem + sidx * kStageBytes, &tmap_kv, &full[sidx], a.k_row0, a.v_row0, tn.block,
+                kvh, a.n_kv_heads);
+    }
+    __syncwarp();
+  }
+  quad_reduce_l(st);
+  const int g = lane >> 2;
+  const int tq = lane & 3;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const int r = g + 8 * half;
+    if (r < wn * a.group) {
+      const int b = first + ws0 + r / a.group;
+      const int h = kvh * a.group + r % a.group;
+      const int64_t pidx = (static_cast<int64_t>(b) * a.max_splits + ps) * hq + h;
+      const float inv = 1.f / st.l[half];
+      float* o = a.o_part + pidx * kHeadDim;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int d = 8 * j + 2 * tq;
+        *reinterpret_cast<float2*>(o + d) =
+            make_float2(st.o[j][2 * half] * inv, st.o[j][2 * half + 1] * inv);
+      }
+      if (tq == 0) a.lse_part[pidx] = st.m[half] + log2f(st.l[half]);
+    }
   }
 }
 
@@ -344,20 +466,39 @@ struct CombineArgs {
   __nv_bfloat16* out;  // [B, Hq, 128]
   int hq;
   int max_splits;
+  int cascade;
+  int slot_off;
 };
 
 __global__ void __launch_bounds__(kHeadDim) decode_combine_kernel(const CombineArgs a) {
   const int b = blockIdx.x;
   const int h = blockIdx.y;
   const int d = threadIdx.x;
-  const int ntiles = num_tiles(__ldg(&a.seq_prefix[b]), __ldg(&a.seq_kvlen[b]));
-  const int ns = (ntiles + kTilesPerSplit - 1) / kTilesPerSplit;
+  const int prefix = __ldg(&a.seq_prefix[b]);
+  const int ntiles = num_tiles(prefix, __ldg(&a.seq_kvlen[b]));
+  // slot ranges: [0, np) prefix partials (cascade), [off, off + ns) context splits
+  int np = 0, off = 0, ns;
+  if (a.cascade) {
+    const int npb = (prefix + kTile - 1) / kTile;
+    np = (npb + kTilesPerSplit - 1) / kTilesPerSplit;
+    off = a.slot_off;
+    ns = (ntiles - npb + kTilesPerSplit - 1) / kTilesPerSplit;
+  } else {
+    ns = (ntiles + kTilesPerSplit - 1) / kTilesPerSplit;
+  }
+  const int64_t base = static_cast<int64_t>(b) * a.max_splits;
   float M = -INFINITY;
-  for (int s = 0; s < ns; ++s)
-    M = fmaxf(M, a.lse_part[(static_cast<int64_t>(b) * a.max_splits + s) * a.hq + h]);
+  for (int s = 0; s < np; ++s) M = fmaxf(M, a.lse_part[(base + s) * a.hq + h]);
+  for (int s = off; s < off + ns; ++s) M = fmaxf(M, a.lse_part[(base + s) * a.hq + h]);
   float L = 0.f, O = 0.f;
-  for (int s = 0; s < ns; ++s) {
-    const int64_t pidx = (static_cast<int64_t>(b) * a.max_splits + s) * a.hq + h;
+  for (int s = 0; s < np; ++s) {
+    const int64_t pidx = (base + s) * a.hq + h;
+    const float w = exp2f(a.lse_part[pidx] - M);
+    L += w;
+    O += w * a.o_part[pidx * kHeadDim + d];
+  }
+  for (int s = off; s < off + ns; ++s) {
+    const int64_t pidx = (base + s) * a.hq + h;
     const float w = exp2f(a.lse_part[pidx] - M);
     L += w;
     O += w * a.o_part[pidx * kHeadDim + d];
@@ -385,7 +526,6 @@ struct PrefillArgs {
   float scale_log2;
 };
 
-constexpr int kPrefillStages = 3;
 
 __global__ void __launch_bounds__(kWarps * 32)
     paged_prefill_kernel(const __grid_constant__ CUtensorMap tmap_kv, const PrefillArgs a) {
@@ -504,11 +644,52 @@ int32_t cortex_paged_decode_attn(const void* tmap_kv, const void* q, const int32
                                  int32_t n_seqs, int32_t n_kv_heads, int32_t group,
                                  int64_t k_row0, int64_t v_row0, float softmax_scale,
                                  float* o_part, float* lse_part, int32_t max_splits, void* out,
-                                 cudaStream_t stream) {
+                                 const int32_t* grp_row, const int32_t* grp_plen,
+                                 const int32_t* grp_first, const int32_t* grp_count,
+                                 int32_t n_groups, int32_t max_group_count,
+                                 int32_t prefix_slots, cudaStream_t stream) {
   if (!tmap_kv || !q || !table || !seq_row || !seq_prefix || !seq_kvlen || !o_part ||
-      !lse_part || !out || n_seqs < 0 || group < 1 || group > 8 || max_splits < 1)
+      !lse_part || !out || n_seqs < 0 || group < 1 || group > 8 || (16 % group) != 0 ||
+      max_splits < 1 || n_groups < 0)
     return CORTEX_EBADARG;
   if (n_seqs == 0) return CORTEX_OK;
+  const int cascade = n_groups > 0 ? 1 : 0;
+  if (cascade && (!grp_row || !grp_plen || !grp_first || !grp_count || prefix_slots < 1 ||
+                  prefix_slots >= max_splits))
+    return CORTEX_EBADARG;
+  const float scale_log2 = softmax_scale * kLog2e;
+  if (cascade) {
+    CascadeArgs c{};
+    c.q = reinterpret_cast<const __nv_bfloat16*>(q);
+    c.table = table;
+    c.table_stride = table_stride;
+    c.grp_row = grp_row;
+    c.grp_plen = grp_plen;
+    c.grp_first = grp_first;
+    c.grp_count = grp_count;
+    c.max_psplits = prefix_slots;
+    c.n_kv_heads = n_kv_heads;
+    c.group = group;
+    c.k_row0 = k_row0;
+    c.v_row0 = v_row0;
+    c.scale_log2 = scale_log2;
+    c.o_part = o_part;
+    c.lse_part = lse_part;
+    c.max_splits = max_splits;
+    const int csmem = kPrefillStages * kStageBytes + 1024 + 256;
+    static bool cconf = false;
+    if (!cconf) {
+      if (cudaFuncSetAttribute(cascade_prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               csmem) != cudaSuccess)
+        return CORTEX_ECUDA;
+      cconf = true;
+    }
+    const int spc = (16 / group) * kWarps;
+    dim3 cgrid((max_group_count + spc - 1) / spc, n_kv_heads, n_groups * prefix_slots);
+    cascade_prefix_kernel<<<cgrid, kWarps * 32, csmem, stream>>>(
+        *reinterpret_cast<const CUtensorMap*>(tmap_kv), c);
+    CORTEX_CHECK_LAUNCH();
+  }
   DecodeArgs a{};
   a.q = reinterpret_cast<const __nv_bfloat16*>(q);
   a.table = table;
@@ -520,10 +701,12 @@ int32_t cortex_paged_decode_attn(const void* tmap_kv, const void* q, const int32
   a.group = group;
   a.k_row0 = k_row0;
   a.v_row0 = v_row0;
-  a.scale_log2 = softmax_scale * kLog2e;
+  a.scale_log2 = scale_log2;
   a.o_part = o_part;
   a.lse_part = lse_part;
   a.max_splits = max_splits;
+  a.cascade = cascade;
+  a.slot_off = cascade ? prefix_slots : 0;
   const int smem = kWarps * kDecodeStages * kStageBytes + 1024 + 256;
   static bool configured = false;
   if (!configured) {
@@ -532,19 +715,21 @@ int32_t cortex_paged_decode_attn(const void* tmap_kv, const void* q, const int32
       return CORTEX_ECUDA;
     configured = true;
   }
-  dim3 grid(max_splits, n_kv_heads, n_seqs);
+  dim3 grid(max_splits - a.slot_off, n_kv_heads, n_seqs);
   paged_decode_kernel<<<grid, kWarps * 32, smem, stream>>>(
       *reinterpret_cast<const CUtensorMap*>(tmap_kv), a);
   CORTEX_CHECK_LAUNCH();
-  CombineArgs c{};
-  c.o_part = o_part;
-  c.lse_part = lse_part;
-  c.seq_prefix = seq_prefix;
-  c.seq_kvlen = seq_kvlen;
-  c.out = reinterpret_cast<__nv_bfloat16*>(out);
-  c.hq = n_kv_heads * group;
-  c.max_splits = max_splits;
-  decode_combine_kernel<<<dim3(n_seqs, c.hq), kHeadDim, 0, stream>>>(c);
+  CombineArgs cb{};
+  cb.o_part = o_part;
+  cb.lse_part = lse_part;
+  cb.seq_prefix = seq_prefix;
+  cb.seq_kvlen = seq_kvlen;
+  cb.out = reinterpret_cast<__nv_bfloat16*>(out);
+  cb.hq = n_kv_heads * group;
+  cb.max_splits = max_splits;
+  cb.cascade = cascade;
+  cb.slot_off = a.slot_off;
+  decode_combine_kernel<<<dim3(n_seqs, cb.hq), kHeadDim, 0, stream>>>(cb);
   CORTEX_CHECK_LAUNCH();
   return CORTEX_OK;
 }

@@ -22,7 +22,7 @@ namespace {
 
 constexpr int kBlockN = 128;  // weight rows per tile (MMA M)
 constexpr int kBlockK = 64;   // K per stage (one 128-byte swizzle row)
-constexpr int kXBox = 32;     // activation rows per TMA box
+constexpr int kXBox = 16;     // activation rows per TMA box
 constexpr int kThreads = 128;
 
 struct GemmArgs {
@@ -49,19 +49,41 @@ struct GemmSmem {
   static constexpr uint32_t kTmemCols = TN < 32 ? 32 : TN;
 };
 
-template <int TN>
-CORTEX_DEVICE void store_cols(const GemmArgs& a, int n, int m_base, const float (&v)[16]) {
+// Final store of rows r0, r0+4, ... < rows of the smem tile: optional fp32 residual,
+// bf16 or fp32 output. Each warp covers one 128-column row with 16-byte accesses;
+// four rows' loads are issued before any store (out may alias residual).
+CORTEX_DEVICE void epilogue_rows(const GemmArgs& a, const float* stile, int m0, int rows, int r0,
+                                 int lane, int col) {
+  for (int rb = r0; rb < rows; rb += 16) {
+    float4 v[4];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int m = m_base + j;
-    if (m < a.M) {
-      float x = v[j];
-      if (a.residual) x += a.residual[static_cast<size_t>(m) * a.ldr + n];
-      if (a.out_f32) {
-        reinterpret_cast<float*>(a.out)[static_cast<size_t>(m) * a.ldo + n] = x;
-      } else {
-        reinterpret_cast<__nv_bfloat16*>(a.out)[static_cast<size_t>(m) * a.ldo + n] =
-            __float2bfloat16_rn(x);
+    for (int u = 0; u < 4; ++u) {
+      const int r = rb + 4 * u;
+      if (r < rows) {
+        v[u] = reinterpret_cast<const float4*>(stile + r * kBlockN)[lane];
+        if (a.residual) {
+          const float4 res = *reinterpret_cast<const float4*>(
+              a.residual + static_cast<size_t>(m0 + r) * a.ldr + col);
+          v[u].x += res.x;
+          v[u].y += res.y;
+          v[u].z += res.z;
+          v[u].w += res.w;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = rb + 4 * u;
+      if (r < rows) {
+        const size_t off = static_cast<size_t>(m0 + r) * a.ldo + col;
+        if (a.out_f32) {
+          *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + off) = v[u];
+        } else {
+          uint2 packed;
+          packed.x = pack_bf16(v[u].x, v[u].y);
+          packed.y = pack_bf16(v[u].z, v[u].w);
+          *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.out) + off) = packed;
+        }
       }
     }
   }
@@ -153,36 +175,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncwarp();
 
-  // ---- epilogue: TMEM -> registers -> global (all 4 warps, thread <-> weight row) ----
+  // ---- epilogue: TMEM -> smem tile [m][128 n] fp32 -> coalesced 16-byte rows ----
+  // (the pipeline stages are free once `done` fired: every MMA, hence every
+  // smem operand read, has completed)
   mbar_wait(done, 0);
   tc_fence_after();
-  const int n = n0 + warp * 32 + lane;
   const uint32_t taddr = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
   const int m_end = min(m0 + TN, args.M);
-
-  if (args.splits == 1) {
-    for (int c0 = 0; c0 < TN && m0 + c0 < m_end; c0 += 16) {
-      uint32_t r[16];
-      tmem_ld_32x32b_x16(taddr + c0, r);
-      tmem_ld_wait();
-      float v[16];
+  const int rows = m_end - m0;
+  float* stile = reinterpret_cast<float*>(smem);
+  for (int c0 = 0; c0 < TN && c0 < rows; c0 += 16) {
+    uint32_t r[16];
+    tmem_ld_32x32b_x16(taddr + c0, r);
+    tmem_ld_wait();
 #pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-      store_cols<TN>(args, n, m0 + c0, v);
-    }
+    for (int j = 0; j < 16; ++j) stile[(c0 + j) * kBlockN + warp * 32 + lane] = __uint_as_float(r[j]);
+  }
+  __syncthreads();
+  // thread -> (row r = tid/32 + 4i, columns 4*lane .. 4*lane+3)
+  const int col = n0 + 4 * lane;
+  const int r0 = threadIdx.x >> 5;
+  if (args.splits == 1) {
+    epilogue_rows(args, stile, m0, rows, r0, lane, col);
   } else {
-    // Split-K: publish this split's fp32 partial, the last CTA of the tile reduces
+    // Split-K: publish this split's fp32 partial; the last CTA of the tile reduces
     // all partials in split order (deterministic) and runs the epilogue.
     float* ws = args.workspace + static_cast<size_t>(split) * args.M * args.N;
-    for (int c0 = 0; c0 < TN && m0 + c0 < m_end; c0 += 16) {
-      uint32_t r[16];
-      tmem_ld_32x32b_x16(taddr + c0, r);
-      tmem_ld_wait();
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int m = m0 + c0 + j;
-        if (m < m_end) __stcg(&ws[static_cast<size_t>(m) * args.N + n], __uint_as_float(r[j]));
-      }
+    for (int r = r0; r < rows; r += 4) {
+      const float4 v = reinterpret_cast<const float4*>(stile + r * kBlockN)[lane];
+      __stcg(reinterpret_cast<float4*>(ws + static_cast<size_t>(m0 + r) * args.N + col), v);
     }
     __threadfence();
     __syncthreads();
@@ -194,20 +215,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     if (*last_flag) {
       __threadfence();
-      for (int c0 = m0; c0 < m_end; c0 += 16) {
-        float v[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = 0.f;
+      for (int r = r0; r < rows; r += 4) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int z = 0; z < args.splits; ++z) {
-          const float* wz = args.workspace + static_cast<size_t>(z) * args.M * args.N;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int m = c0 + j;
-            if (m < m_end) v[j] += __ldcg(&wz[static_cast<size_t>(m) * args.N + n]);
-          }
+          const float4 v = __ldcg(reinterpret_cast<const float4*>(
+              args.workspace + (static_cast<size_t>(z) * args.M + m0 + r) * args.N + col));
+          acc.x += v.x;
+          acc.y += v.y;
+          acc.z += v.z;
+          acc.w += v.w;
         }
-        store_cols<TN>(args, n, c0, v);
+        reinterpret_cast<float4*>(stile + r * kBlockN)[lane] = acc;
       }
+      __syncwarp();
+      epilogue_rows(args, stile, m0, rows, r0, lane, col);
       if (threadIdx.x == 0) args.counters[tile_id] = 0;
     }
   }
@@ -253,7 +274,32 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 
 }  // namespace
 
+int32_t cortex_gemm_2sm_launch(const void* tmap_w, const void* tmap_x, int32_t M, int32_t N,
+                               int32_t K, void* out, int32_t ldo, int32_t out_f32,
+                               const void* residual, int32_t ldr, cudaStream_t stream);
+
+namespace {
+int g_gemm_mode = 0;  // 0 auto, 1 force the 1-SM (split-K) kernel, 2 force 2-SM when legal
+}
+
 extern "C" {
+
+// Kernel choice: 1 = 1-SM swap-AB kernel with split-K (decode-sized, weight-streaming
+// bound), 2 = persistent 2-SM kernel (M > 128, compute bound; needs N % 256 == 0).
+int32_t cortex_gemm_path(int32_t M, int32_t N, int32_t K) {
+  (void)K;
+  const bool legal2 = (N % 256) == 0;
+  if (g_gemm_mode == 1 || !legal2) return 1;
+  if (g_gemm_mode == 2) return 2;
+  return M > 128 ? 2 : 1;
+}
+
+// Test hook: 0 auto, 1 force 1-SM, 2 force 2-SM.
+int32_t cortex_gemm_set_mode(int32_t mode) {
+  if (mode < 0 || mode > 2) return CORTEX_EBADARG;
+  g_gemm_mode = mode;
+  return CORTEX_OK;
+}
 
 // Encode a 2-D bf16 TMA descriptor (128 bytes, written to tmap_out) over a
 // row-major matrix [rows, cols] with the given row pitch. box_cols * 2 must be
@@ -306,6 +352,9 @@ int32_t cortex_gemm_bf16(const void* tmap_w, const void* tmap_x, int32_t M, int3
                          int32_t* counters, int32_t n_counters, cudaStream_t stream) {
   if (!tmap_w || !tmap_x || !out || M <= 0 || N <= 0 || K <= 0 || N % kBlockN || K % kBlockK)
     return CORTEX_EBADARG;
+  if (cortex_gemm_path(M, N, K) == 2)
+    return cortex_gemm_2sm_launch(tmap_w, tmap_x, M, N, K, out, ldo, out_f32, residual, ldr,
+                                  stream);
   GemmArgs a{};
   a.M = M;
   a.N = N;

@@ -432,7 +432,9 @@ class GpuEngineState:
                     allocs.append((c.slot, _blocks(c.prefix_len) + j // BLOCK_TOKENS, 1))
                     c.priv_blocks += 1
                 kv_len = c.prefix_len + j + 1
-                toks.append(DecodeTok(c.slot, c.prefix_len, kv_len, hist_pos=c.have))
+                pre = self.resident.get(c.stage_id)
+                toks.append(DecodeTok(c.slot, c.prefix_len, kv_len, hist_pos=c.have,
+                                      prefix_key=pre.row if pre is not None else -1))
             self._alloc(allocs)
             self.worker.forward_decode(toks)
             for c in step:

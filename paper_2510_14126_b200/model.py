@@ -196,6 +196,7 @@ class GpuWorker:
         self.steps = 0
         self.on_forward = None  # optional hook(plan, n_out) for parity checking
         self.prof: KernelProfile | None = None  # optional per-kernel-class CUDA-event timing
+        self.cascade = True  # shared-prefix decode attention (prefix KV read once per step)
 
     # ------------------------------------------------------------------ helpers
 
@@ -292,6 +293,17 @@ class GpuWorker:
         dec_prefix = np.empty(n_dec, i32)
         dec_kvlen = np.empty(n_dec, i32)
         out_rows, out_slot, out_hist = [], [], []
+        # shared-prefix (cascade) groups: calls on the same resident prefix made contiguous
+        groups = []
+        if n_dec and self.cascade and all(d.prefix_key >= 0 for d in plan.decode if d.prefix_len):
+            plan.decode.sort(key=lambda d: d.prefix_key if d.prefix_len else -1)
+            for i, d in enumerate(plan.decode):
+                if not d.prefix_len:
+                    continue
+                if groups and groups[-1][0] == d.prefix_key:
+                    groups[-1][3] += 1
+                else:
+                    groups.append([d.prefix_key, d.prefix_len, i, 1])
         for i, d in enumerate(plan.decode):
             p = d.kv_len - 1
             c, o = token_slot(d.prefix_len, p)
@@ -336,14 +348,27 @@ class GpuWorker:
         n_out = len(out_rows)
         if n_out > self.max_out:
             raise ValueError("too many output rows in one step")
+        garr = np.asarray(groups, i32).reshape(-1, 4).T.copy() if groups else np.zeros((4, 0), i32)
         (d_pos, d_arow, d_acol, d_aoff, d_tok, d_drow, d_dpre, d_dkv, d_prow, d_ppre, d_pkv,
-         d_pqs, d_pql, d_orow, d_oslot, d_ohist) = self._upload([
+         d_pqs, d_pql, d_orow, d_oslot, d_ohist, d_grow, d_gplen, d_gfirst, d_gcount) = self._upload([
             pos, app_row, app_col, app_off, tok_ids, dec_row, dec_prefix, dec_kvlen, pf_row,
             pf_prefix, pf_kvlen, pf_qstart, pf_qlen, np.asarray(out_rows, i32),
-            np.asarray(out_slot, i32), np.asarray(out_hist, i32)])
+            np.asarray(out_slot, i32), np.asarray(out_hist, i32), garr[0], garr[1], garr[2],
+            garr[3]])
         max_splits = 1
+        dec_groups = None
         if n_dec:
-            max_splits = max(ops.decode_splits(int(a), int(b)) for a, b in zip(dec_prefix, dec_kvlen))
+            if groups:
+                npb = (dec_prefix + BLOCK_TOKENS - 1) // BLOCK_TOKENS
+                ntl = npb + (dec_kvlen - dec_prefix + BLOCK_TOKENS - 1) // BLOCK_TOKENS
+                priv = int(((ntl - npb + 15) // 16).max())
+                pslots = int(((garr[1] + BLOCK_TOKENS - 1) // BLOCK_TOKENS + 15).max() // 16)
+                max_splits = pslots + priv
+                dec_groups = (d_grow, d_gplen, d_gfirst, d_gcount, len(groups), int(garr[3].max()),
+                              pslots)
+            else:
+                max_splits = max(ops.decode_splits(int(a), int(b))
+                                 for a, b in zip(dec_prefix, dec_kvlen))
             if max_splits > self.max_splits:
                 raise ValueError("decode context exceeds max_seq_tokens")
         w, wm = self.w, self.wmap
@@ -391,7 +416,7 @@ class GpuWorker:
                 e0 = prof.open("attn_decode") if prof is not None else None
                 ops.paged_decode_attn(self.kvmap, self.q, self.table, d_drow, d_dpre, d_dkv, n_dec,
                                       hkv, cfg.group, k0, v0, self.scale, o_part, lse_part,
-                                      max_splits, self.attn)
+                                      max_splits, self.attn, groups=dec_groups)
                 if e0 is not None:
                     prof.close("attn_decode", e0, dec_bytes, dec_flops)
                 nl += 2

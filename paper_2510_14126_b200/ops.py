@@ -69,7 +69,7 @@ def weight_map(w: torch.Tensor) -> TensorMap:
 
 
 def act_map(x: torch.Tensor) -> TensorMap:
-    return TensorMap(x, 32)
+    return TensorMap(x, 16)
 
 
 def kv_map(cache2d: torch.Tensor) -> TensorMap:
@@ -86,6 +86,14 @@ class GemmWorkspace:
 
 def gemm_splits(M: int, N: int, K: int) -> int:
     return int(lib().cortex_gemm_splits(M, N, K))
+
+
+def gemm_path(M: int, N: int, K: int) -> int:
+    return int(lib().cortex_gemm_path(M, N, K))
+
+
+def gemm_set_mode(mode: int) -> None:
+    _check(lib().cortex_gemm_set_mode(mode), "cortex_gemm_set_mode")
 
 
 def gemm(wmap: TensorMap, xmap: TensorMap, M: int, out: torch.Tensor, ws: GemmWorkspace,
@@ -158,13 +166,19 @@ def decode_splits(prefix_len: int, kv_len: int) -> int:
 
 def paged_decode_attn(kvmap: TensorMap, q, table, seq_row, seq_prefix, seq_kvlen, n_seqs,
                       n_kv_heads, group, k_row0, v_row0, scale, o_part, lse_part, max_splits, out,
-                      stream=None) -> None:
+                      groups=None, stream=None) -> None:
+    """groups: None, or (grp_row, grp_plen, grp_first, grp_count, n_groups, max_count,
+    prefix_slots) for shared-prefix (cascade) attention."""
+    if groups is None:
+        g = (None, None, None, None, 0, 0, 0)
+    else:
+        g = (_ptr(groups[0]), _ptr(groups[1]), _ptr(groups[2]), _ptr(groups[3])) + tuple(groups[4:])
     _check(
         lib().cortex_paged_decode_attn(
             kvmap.ptr, q.data_ptr(), table.data_ptr(), table.stride(0), seq_row.data_ptr(),
             seq_prefix.data_ptr(), seq_kvlen.data_ptr(), n_seqs, n_kv_heads, group, k_row0,
             v_row0, scale, o_part.data_ptr(), lse_part.data_ptr(), max_splits, out.data_ptr(),
-            _stream(stream),
+            *g, _stream(stream),
         ),
         "cortex_paged_decode_attn",
     )

@@ -75,17 +75,46 @@ def test_gemm_residual_and_f32(cuda, M):
     assert rel(out32, x[:M].float() @ w.float().T) < 1e-5
 
 
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("M,N,K", [(129, 512, 256), (700, 4096, 4096), (300, 6144, 4096),
+                                   (2048, 1536, 256), (33, 1024, 768), (1000, 28672, 4096),
+                                   (4096, 4096, 14336), (5, 256, 4096)])
+def test_gemm_paths_match(cuda, mode, M, N, K):
+    """Both kernels (1-SM split-K and persistent 2-SM cta_group::2) on the same problems."""
+    o = ops()
+    g = torch.Generator(device=cuda).manual_seed(M + N)
+    x = torch.randn(max(M, 32), K, generator=g, device=cuda).to(torch.bfloat16)
+    w = (torch.randn(N, K, generator=g, device=cuda) * 0.05).to(torch.bfloat16)
+    r = torch.randn(M, N, generator=g, device=cuda)
+    ws = o.GemmWorkspace(cuda)
+    o.gemm_set_mode(mode)
+    try:
+        out = torch.full((M, N), float("nan"), device=cuda, dtype=torch.bfloat16)
+        o.gemm(o.weight_map(w), o.act_map(x), M, out, ws)
+        out32 = torch.empty(M, N, device=cuda)
+        o.gemm(o.weight_map(w), o.act_map(x), M, out32, ws, residual=r)
+        torch.cuda.synchronize()
+    finally:
+        o.gemm_set_mode(0)
+    ref = x[:M].float() @ w.float().T
+    assert torch.isfinite(out.float()).all()
+    assert rel(out, ref) < 4e-3
+    assert rel(out32, ref + r) < 4e-5  # fp32 accumulation order over K <= 14336
+
+
 def test_gemm_batch_invariant(cuda):
-    """A row's result does not depend on the other rows of a decode batch (M <= 256)."""
+    """Within the decode regime (M <= 128, the 1-SM kernel, split-K fixed by N and K) a
+    row's result does not depend on the other rows of the batch."""
     o = ops()
     N, K = 6144, 4096
     g = torch.Generator(device=cuda).manual_seed(3)
-    x = torch.randn(256, K, generator=g, device=cuda).to(torch.bfloat16)
+    x = torch.randn(128, K, generator=g, device=cuda).to(torch.bfloat16)
     w = (torch.randn(N, K, generator=g, device=cuda) * 0.05).to(torch.bfloat16)
     ws = o.GemmWorkspace(cuda)
-    full = torch.empty(256, N, device=cuda, dtype=torch.bfloat16)
-    o.gemm(o.weight_map(w), o.act_map(x), 256, full, ws)
-    for m in (1, 17, 64, 130):
+    full = torch.empty(128, N, device=cuda, dtype=torch.bfloat16)
+    assert o.gemm_path(128, N, K) == 1
+    o.gemm(o.weight_map(w), o.act_map(x), 128, full, ws)
+    for m in (1, 17, 64, 100):
         part = torch.empty(m, N, device=cuda, dtype=torch.bfloat16)
         o.gemm(o.weight_map(w), o.act_map(x), m, part, ws)
         assert torch.equal(part, full[:m])
@@ -168,6 +197,66 @@ def test_paged_decode_attention(cuda, group):
             ref = attention_ref(q[b:b + 1].float().cpu(), k, v, torch.tensor([kvlen - 1]),
                                 torch.arange(kvlen))
             assert rel(out[b:b + 1], ref) < 4e-3, (layer, b, prefix, kvlen)
+
+
+@pytest.mark.parametrize("group", [4, 2])
+@pytest.mark.parametrize("plens", [(1000, 40), (8192,), (16, 5, 0)])
+def test_cascade_decode_attention(cuda, group, plens):
+    """Shared-prefix decode: calls grouped by resident prefix, prefix attended once."""
+    o = ops()
+    hkv, nb = 2, 2048
+    hq = hkv * group
+    cache = _make_cache(cuda, 1, nb, hkv, seed=31 + group)
+    rng = np.random.default_rng(7)
+    perm = list(rng.permutation(nb))
+    # per prefix: (table row, blocks); then calls: 1..37 per group with ragged private lengths
+    n_groups = len(plens)
+    counts = [37, 3, 1][:n_groups]
+    rows_total = n_groups + sum(counts)
+    table = torch.zeros(rows_total, 600, dtype=torch.int32)
+    pref_blocks = []
+    for g, P in enumerate(plens):
+        npb = (P + 15) // 16
+        ids = [perm.pop() for _ in range(npb)]
+        table[g, :npb] = torch.tensor(ids, dtype=torch.int32)
+        pref_blocks.append(ids)
+    seq_row, seq_pre, seq_kv, grp = [], [], [], []
+    r = n_groups
+    for g, P in enumerate(plens):
+        first = len(seq_row)
+        for i in range(counts[g]):
+            priv = int(rng.integers(1, 300))
+            npr = (priv + 15) // 16
+            ids = pref_blocks[g] + [perm.pop() for _ in range(npr)]
+            table[r, :len(ids)] = torch.tensor(ids, dtype=torch.int32)
+            seq_row.append(r)
+            seq_pre.append(P)
+            seq_kv.append(P + priv)
+            r += 1
+        if P:
+            grp.append((g, P, first, counts[g]))
+    B = len(seq_row)
+    dev = lambda a: torch.as_tensor(np.asarray(a, dtype=np.int32), device=cuda)
+    table = table.to(cuda)
+    pslots = max([((P + 15) // 16 + 15) // 16 for _, P, _, _ in grp] + [1])
+    priv = max(((kv - p) + 255) // 256 for p, kv in zip(seq_pre, seq_kv))
+    max_splits = pslots + priv
+    q = torch.randn(B, hq, 128, device=cuda).to(torch.bfloat16)
+    o_part = torch.empty(B, max_splits, hq, 128, device=cuda)
+    lse_part = torch.empty(B, max_splits, hq, device=cuda)
+    out = torch.empty(B, hq, 128, device=cuda, dtype=torch.bfloat16)
+    ga = np.asarray(grp, dtype=np.int32).reshape(-1, 4).T
+    groups = (dev(ga[0]), dev(ga[1]), dev(ga[2]), dev(ga[3]), len(grp), int(ga[3].max()), pslots)
+    k0, v0 = _rows(0, nb, hkv)
+    o.paged_decode_attn(o.kv_map(cache.view(-1, 128)), q, table, dev(seq_row), dev(seq_pre),
+                        dev(seq_kv), B, hkv, group, k0, v0, 1 / math.sqrt(128), o_part, lse_part,
+                        max_splits, out, groups=groups)
+    torch.cuda.synchronize()
+    for b in range(B):
+        k, v = _logical_kv(cache, 0, table[seq_row[b]].cpu(), seq_pre[b], seq_kv[b])
+        ref = attention_ref(q[b:b + 1].float().cpu(), k, v, torch.tensor([seq_kv[b] - 1]),
+                            torch.arange(seq_kv[b]))
+        assert rel(out[b:b + 1], ref) < 4e-3, (b, seq_pre[b], seq_kv[b])
 
 
 @pytest.mark.parametrize("group", [4, 2])
