@@ -149,7 +149,33 @@ int32_t cortex_paged_decode_attn(const void* tmap_kv, const void* q, const int32
                                  const int32_t* grp_row, const int32_t* grp_plen,
                                  const int32_t* grp_first, const int32_t* grp_count,
                                  int32_t n_groups, int32_t max_group_count,
-                                 int32_t prefix_slots, cortex_stream_t stream);
+                                 int32_t prefix_slots, const void* tmap_q,
+                                 cortex_stream_t stream);
+
+/* TMA descriptor over q [n_tok, hq, 128] (box 64 dims x group heads x 128/group tokens)
+ * for the tensor-core attention kernels; tmap_q above selects the tcgen05 cascade pass. */
+int32_t cortex_tmap_encode_q(void* tmap_out, const void* q, uint64_t n_tok, int32_t hq,
+                             int32_t group);
+
+/* tcgen05 flash attention, 128 query rows (tokens x GQA group) per CTA, paged K/V in
+ * 8-block key tiles, TMEM S/O accumulators. Prefill: same contract as
+ * cortex_paged_prefill_attn. Cascade: the shared-prefix pass of decode (partials into
+ * slots [0, prefix_slots) of o_part / lse_part, rows = decode index). */
+int32_t cortex_fmha_prefill_tc(const void* tmap_kv, const void* tmap_q, void* out,
+                               const int32_t* table, int32_t table_stride, const int32_t* seq_row,
+                               const int32_t* seq_prefix, const int32_t* seq_kvlen,
+                               const int32_t* seq_qstart, const int32_t* seq_qlen, int32_t n_seqs,
+                               int32_t max_qlen, int32_t n_kv_heads, int32_t group,
+                               int64_t k_row0, int64_t v_row0, float softmax_scale,
+                               cortex_stream_t stream);
+int32_t cortex_fmha_cascade_tc(const void* tmap_kv, const void* tmap_q, const int32_t* table,
+                               int32_t table_stride, const int32_t* grp_row,
+                               const int32_t* grp_plen, const int32_t* grp_first,
+                               const int32_t* grp_count, int32_t n_groups, int32_t max_count,
+                               int32_t prefix_slots, int32_t n_kv_heads, int32_t group,
+                               int64_t k_row0, int64_t v_row0, float softmax_scale,
+                               float* o_part, float* lse_part, int32_t max_splits,
+                               cortex_stream_t stream);
 
 /* Paged prefill attention: the last seq_qlen[s] positions of each sequence
  * attend causally to its prefix + private tokens. */

@@ -647,7 +647,7 @@ int32_t cortex_paged_decode_attn(const void* tmap_kv, const void* q, const int32
                                  const int32_t* grp_row, const int32_t* grp_plen,
                                  const int32_t* grp_first, const int32_t* grp_count,
                                  int32_t n_groups, int32_t max_group_count,
-                                 int32_t prefix_slots, cudaStream_t stream) {
+                                 int32_t prefix_slots, const void* tmap_q, cudaStream_t stream) {
   if (!tmap_kv || !q || !table || !seq_row || !seq_prefix || !seq_kvlen || !o_part ||
       !lse_part || !out || n_seqs < 0 || group < 1 || group > 8 || (16 % group) != 0 ||
       max_splits < 1 || n_groups < 0)
@@ -658,7 +658,13 @@ int32_t cortex_paged_decode_attn(const void* tmap_kv, const void* q, const int32
                   prefix_slots >= max_splits))
     return CORTEX_EBADARG;
   const float scale_log2 = softmax_scale * kLog2e;
-  if (cascade) {
+  if (cascade && tmap_q) {
+    const int32_t rc = cortex_fmha_cascade_tc(
+        tmap_kv, tmap_q, table, table_stride, grp_row, grp_plen, grp_first, grp_count, n_groups,
+        max_group_count, prefix_slots, n_kv_heads, group, k_row0, v_row0, softmax_scale, o_part,
+        lse_part, max_splits, stream);
+    if (rc != CORTEX_OK) return rc;
+  } else if (cascade) {
     CascadeArgs c{};
     c.q = reinterpret_cast<const __nv_bfloat16*>(q);
     c.table = table;

@@ -1,0 +1,553 @@
+// Tensor-core (tcgen05) paged flash attention for the many-query cases:
+//   * prompt / stage-prefix prefill (causal over prefix + own tokens), and
+//   * the shared-prefix ("cascade") pass of decode: all decode queries of the
+//     calls on one resident stage prefix against that prefix.
+//
+// One CTA = 128 query rows (128/group query tokens x the GQA group of q heads
+// that share one kv head) against a range of KV blocks of one block-table row.
+// Key tiles are 8 paged blocks (<= 128 keys); a block may be partial (the last
+// prefix block when P % 16 != 0, the last private block), so every key column
+// carries (position, valid) from its block descriptor.
+//
+//   warp 0      TMA producer: Q once (3-D map: tokens x heads x dims), then per
+//               key tile 8 blocks x {K lo, K hi, V lo, V hi} 64-column boxes into a
+//               2-stage ring (128-byte swizzle)
+//   warp 1      MMA issuer (one thread): S_t = Q K_t^T  (M=128, N=128, K=128) into
+//               one of two TMEM S buffers; O += P_{t-1} V_{t-1}  (A = P from smem,
+//               K-major; B = V from smem, MN-major) into the TMEM O accumulator
+//   warps 2..5  softmax: thread = query row = TMEM lane; S row -> mask -> running
+//               max (rescale O in TMEM only when the max grows by > 2^8) -> P (bf16)
+//               into smem -> final O / l (bf16 output, or fp32 partial + LSE)
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int kHD = 128;
+constexpr int kBlk = 16;
+constexpr int kBlocksPerTile = 8;  // 128 keys
+constexpr int kRows = 128;
+constexpr int kThreadsTC = 192;
+constexpr float kLog2eTC = 1.4426950408889634f;
+constexpr float kRescaleThresh = 8.0f;  // log2 units
+
+constexpr int kQBytes = kRows * kHD * 2;                 // 32 KiB
+constexpr int kKVHalf = kBlocksPerTile * kBlk * 64 * 2;  // 16 KiB  [128 keys x 64 dims]
+constexpr int kKVStage = 4 * kKVHalf;                    // K lo, K hi, V lo, V hi
+constexpr int kPBytes = kRows * 128 * 2;                 // 32 KiB
+constexpr int kStagesTC = 2;
+constexpr int kOffQ = 0;
+constexpr int kOffKV = kQBytes;
+constexpr int kOffP = kOffKV + kStagesTC * kKVStage;
+constexpr int kOffBar = kOffP + 2 * kPBytes;  // P hi, P lo
+constexpr int kSmemTC = kOffBar + 256 + 1024;
+constexpr uint32_t kTmemColsTC = 512;  // S0 [0,128) S1 [128,256) O [256,384)
+
+struct FmhaArgs {
+  const int* table;
+  int table_stride;
+  int n_kv_heads;
+  int group;
+  int64_t k_row0, v_row0;
+  float scale_log2;
+  int mode;  // 0: prefill (final bf16 output), 1: cascade prefix (fp32 partial + LSE)
+  // prefill
+  const int* seq_row;
+  const int* seq_prefix;
+  const int* seq_kvlen;
+  const int* seq_qstart;
+  const int* seq_qlen;
+  __nv_bfloat16* out;
+  // cascade
+  const int* grp_row;
+  const int* grp_plen;
+  const int* grp_first;
+  const int* grp_count;
+  int max_psplits;
+  float* o_part;
+  float* lse_part;
+  int max_splits;
+};
+
+struct BlockRef {
+  int block, pos0, nvalid;
+};
+
+CORTEX_DEVICE BlockRef block_ref(const int* table_row, int prefix_len, int kv_len, int j,
+                                 int blk_end) {
+  BlockRef r;
+  const int npb = (prefix_len + kBlk - 1) / kBlk;
+  if (j >= blk_end) {
+    r.block = __ldg(&table_row[0]);  // finite data, fully masked
+    r.pos0 = 0;
+    r.nvalid = 0;
+    return r;
+  }
+  r.block = __ldg(&table_row[j]);
+  if (j < npb) {
+    r.pos0 = j * kBlk;
+    r.nvalid = min(kBlk, prefix_len - j * kBlk);
+  } else {
+    const int jj = j - npb;
+    r.pos0 = prefix_len + jj * kBlk;
+    r.nvalid = min(kBlk, kv_len - prefix_len - jj * kBlk);
+  }
+  return r;
+}
+
+CORTEX_DEVICE void tma_load_3d(void* smem_dst, const void* desc, uint64_t* bar, int c0, int c1,
+                               int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+// MN-major, 128-byte-swizzled operand: rows of 128 B along K, 64-element atoms along MN
+// `lbo` bytes apart, 8-row groups along K 1024 bytes apart.
+CORTEX_DEVICE uint64_t umma_desc_sw128_mn(uint32_t smem_addr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
+
+CORTEX_DEVICE void tmem_ld_x32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32"
+      " {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15,"
+      " %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+CORTEX_DEVICE void tmem_st_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0],"
+      " {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16,"
+      " %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};\n" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+      "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+      "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
+CORTEX_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
+// mbarrier wait that traps (with a diagnostic) instead of hanging forever when a
+// phase never completes (~4 s): a logic error must not wedge the GPU.
+CORTEX_DEVICE void mbar_wait_guard(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  const long long t0 = clock64();
+  while (true) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (clock64() - t0 > (8ll << 30)) {
+      printf("fmha_tc hang: block (%d,%d,%d) thread %d barrier smem+%u parity %u\n", blockIdx.x,
+             blockIdx.y, blockIdx.z, threadIdx.x, addr & 0xffff, parity);
+      __trap();
+    }
+  }
+}
+
+CORTEX_DEVICE void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kThreadsTC, 1)
+    fmha_tc_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                   const __grid_constant__ CUtensorMap tmap_kv, const FmhaArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;    // [2]
+  uint64_t* p_full = bars + 7;
+  uint64_t* p_empty = bars + 8;
+  uint64_t* o_done = bars + 9;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 10);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int qb = blockIdx.x;
+  const int kvh = blockIdx.y;
+  const int item = blockIdx.z;
+  const int group = a.group;
+  const int tpb = kRows / group;  // query tokens per CTA
+
+  // ---- work item ----
+  int row, prefix_len, kv_len, tok0, ntok, qpos_base, blk_begin, blk_end;
+  if (a.mode == 0) {
+    const int qlen = __ldg(&a.seq_qlen[item]);
+    if (qb * tpb >= qlen) return;
+    row = __ldg(&a.seq_row[item]);
+    prefix_len = __ldg(&a.seq_prefix[item]);
+    kv_len = __ldg(&a.seq_kvlen[item]);
+    tok0 = __ldg(&a.seq_qstart[item]) + qb * tpb;
+    ntok = min(tpb, qlen - qb * tpb);
+    qpos_base = kv_len - qlen + qb * tpb;
+    const int last = qpos_base + ntok - 1;  // keys needed: positions <= last
+    const int npb = (prefix_len + kBlk - 1) / kBlk;
+    blk_begin = 0;
+    blk_end = last < prefix_len ? last / kBlk + 1 : npb + (last - prefix_len) / kBlk + 1;
+  } else {
+    const int g = item / a.max_psplits;
+    const int ps = item % a.max_psplits;
+    const int count = __ldg(&a.grp_count[g]);
+    if (qb * tpb >= count) return;
+    row = __ldg(&a.grp_row[g]);
+    prefix_len = __ldg(&a.grp_plen[g]);
+    kv_len = prefix_len;
+    const int npb = (prefix_len + kBlk - 1) / kBlk;
+    blk_begin = ps * 16;  // the decode kernels' 16-block split granularity
+    if (blk_begin >= npb) return;
+    blk_end = min(npb, blk_begin + 16);
+    tok0 = __ldg(&a.grp_first[g]) + qb * tpb;
+    ntok = min(tpb, count - qb * tpb);
+    qpos_base = 0x3fffffff;  // decode queries follow the whole prefix
+  }
+  const int n_kt = (blk_end - blk_begin + kBlocksPerTile - 1) / kBlocksPerTile;
+  const int* table_row = a.table + static_cast<int64_t>(row) * a.table_stride;
+  const int hq = a.n_kv_heads * group;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_q);
+    tma_prefetch_desc(&tmap_kv);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < kStagesTC; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+    }
+    mbar_init(p_full, 4);
+    mbar_init(p_empty, 1);
+    mbar_init(o_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_holder, kTmemColsTC);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  const uint32_t tmem_s = tmem;         // S buffer b at +128*b
+  const uint32_t tmem_o = tmem + 256;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      // ---- producer ----
+      mbar_arrive_expect_tx(q_full, kQBytes);
+      tma_load_3d(smem + kOffQ, &tmap_q, q_full, 0, kvh * group, tok0);
+      tma_load_3d(smem + kOffQ + kQBytes / 2, &tmap_q, q_full, 64, kvh * group, tok0);
+      for (int kt = 0; kt < n_kt; ++kt) {
+        const int s = kt % kStagesTC;
+        const uint32_t ph = (kt / kStagesTC) & 1;
+        mbar_wait_guard(&kv_empty[s], ph ^ 1);
+        uint8_t* st = smem + kOffKV + s * kKVStage;
+        mbar_arrive_expect_tx(&kv_full[s], kKVStage);
+        for (int j = 0; j < kBlocksPerTile; ++j) {
+          const BlockRef b = block_ref(table_row, prefix_len, kv_len,
+                                       blk_begin + kt * kBlocksPerTile + j, blk_end);
+          const int64_t r = (static_cast<int64_t>(b.block) * a.n_kv_heads + kvh) * kBlk;
+          const int off = j * kBlk * 128;
+          tma_load_2d(st + 0 * kKVHalf + off, &tmap_kv, &kv_full[s], 0, static_cast<int>(a.k_row0 + r));
+          tma_load_2d(st + 1 * kKVHalf + off, &tmap_kv, &kv_full[s], 64, static_cast<int>(a.k_row0 + r));
+          tma_load_2d(st + 2 * kKVHalf + off, &tmap_kv, &kv_full[s], 0, static_cast<int>(a.v_row0 + r));
+          tma_load_2d(st + 3 * kKVHalf + off, &tmap_kv, &kv_full[s], 64, static_cast<int>(a.v_row0 + r));
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      // ---- MMA issuer ----
+      constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128);
+      constexpr uint32_t idesc_pv = umma_idesc_bf16(128, 128) | (1u << 16);  // B (V) MN-major
+      const uint32_t q_addr = smem_u32(smem + kOffQ);
+      const uint32_t p_addr = smem_u32(smem + kOffP);
+      mbar_wait_guard(q_full, 0);
+      for (int kt = 0; kt <= n_kt; ++kt) {
+        if (kt < n_kt) {
+          const int s = kt % kStagesTC;
+          const uint32_t ph = (kt / kStagesTC) & 1;
+          mbar_wait_guard(&kv_full[s], ph);
+          tc_fence_after();
+          const uint32_t k_addr = smem_u32(smem + kOffKV + s * kKVStage);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t off = (kk >> 2) * kKVHalf + (kk & 3) * 32;
+            umma_bf16_ss(tmem_s + 128 * s, umma_desc_sw128(q_addr + off),
+                         umma_desc_sw128(k_addr + off), idesc_s, kk != 0 ? 1u : 0u);
+          }
+          umma_commit(&s_full[s]);
+        }
+        if (kt > 0) {
+          const int t = kt - 1;
+          const int s = t % kStagesTC;
+          mbar_wait_guard(p_full, t & 1);
+          tc_fence_after();
+          const uint32_t v_addr = smem_u32(smem + kOffKV + s * kKVStage + 2 * kKVHalf);
+          // O += P_hi V + P_lo V  (P = P_hi + P_lo to ~2^-17)
+#pragma unroll
+          for (int part = 0; part < 2; ++part) {
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              umma_bf16_ss(tmem_o,
+                           umma_desc_sw128(p_addr + part * kPBytes + (kk >> 2) * kKVHalf +
+                                           (kk & 3) * 32),
+                           umma_desc_sw128_mn(v_addr + kk * 2048, kKVHalf), idesc_pv,
+                           (t | kk | part) != 0 ? 1u : 0u);
+            }
+          }
+          umma_commit(&kv_empty[s]);
+          umma_commit(p_empty);
+          if (t == n_kt - 1) umma_commit(o_done);
+        }
+      }
+    }
+  } else {
+    // ---- softmax warps: thread <-> query row (TMEM lane) ----
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const bool row_ok = r < ntok * group;
+    const int qpos = qpos_base + r / group;
+    float m_run = -INFINITY, l_run = 0.f;
+    uint8_t* psm = smem + kOffP;
+    for (int kt = 0; kt < n_kt; ++kt) {
+      const int s = kt % kStagesTC;
+      mbar_wait_guard(&s_full[s], (kt / kStagesTC) & 1);
+      tc_fence_after();
+      float sv[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t u[32];
+        tmem_ld_x32(tmem_s + 128 * s + lane_off + 32 * c, u);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) sv[32 * c + i] = __uint_as_float(u[i]);
+      }
+      // mask + tile max
+      float mt = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < kBlocksPerTile; ++j) {
+        const BlockRef b = block_ref(table_row, prefix_len, kv_len,
+                                     blk_begin + kt * kBlocksPerTile + j, blk_end);
+#pragma unroll
+        for (int i = 0; i < kBlk; ++i) {
+          const bool ok = row_ok && i < b.nvalid && b.pos0 + i <= qpos;
+          const float v = ok ? sv[kBlk * j + i] * a.scale_log2 : -INFINITY;
+          sv[kBlk * j + i] = v;
+          mt = fmaxf(mt, v);
+        }
+      }
+      // wait until PV of the previous tile finished (P smem free, O stable)
+      if (kt > 0) mbar_wait_guard(p_empty, (kt - 1) & 1);
+      tc_fence_after();
+      // running max: adopt the tile max when the row had none yet (its O row is 0), or
+      // when it grew by more than 2^8 (then O and l are rescaled); otherwise keep the
+      // stale max (p <= 2^8, exact after the final 1/l).
+      const bool adopt = mt > -INFINITY && (m_run == -INFINITY || mt > m_run + kRescaleThresh);
+      const float alpha = !adopt ? 1.f : (m_run == -INFINITY ? 0.f : exp2f(m_run - mt));
+      // O rescale (tcgen05.ld/st are warp-collective: decided per warp, alpha per row)
+      if (kt > 0 && __any_sync(0xffffffffu, adopt && m_run != -INFINITY)) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t u[32];
+          tmem_ld_x32(tmem_o + lane_off + 32 * c, u);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * alpha);
+          tmem_st_x32(tmem_o + lane_off + 32 * c, u);
+        }
+        tmem_st_wait();
+      }
+      if (adopt) {
+        l_run *= alpha;
+        m_run = mt;
+      }
+      const float m_use = m_run == -INFINITY ? 0.f : m_run;
+      // P = exp2(s - m) -> bf16 row into the swizzled K-major P tile
+#pragma unroll
+      for (int ch = 0; ch < 16; ++ch) {
+        float p[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          p[e] = exp2f(sv[8 * ch + e] - m_use);
+          l_run += p[e];
+        }
+        uint4 hi, lo;
+        split_bf16(p[0], p[1], hi.x, lo.x);
+        split_bf16(p[2], p[3], hi.y, lo.y);
+        split_bf16(p[4], p[5], hi.z, lo.z);
+        split_bf16(p[6], p[7], hi.w, lo.w);
+        const int half = ch >> 3;
+        const uint32_t off = half * kKVHalf + sw128_offset(r, ch & 7);
+        *reinterpret_cast<uint4*>(psm + off) = hi;
+        *reinterpret_cast<uint4*>(psm + kPBytes + off) = lo;
+      }
+      fence_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    // ---- epilogue ----
+    mbar_wait_guard(o_done, 0);
+    tc_fence_after();
+    const int tok = tok0 + r / group;
+    const int h = kvh * group + r % group;
+    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+    if (a.mode == 0) {
+      __nv_bfloat16* orow = a.out + (static_cast<int64_t>(tok) * hq + h) * kHD;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t u[32];
+        tmem_ld_x32(tmem_o + lane_off + 32 * c, u);
+        tmem_ld_wait();
+        if (row_ok) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            uint4 v;
+            v.x = pack_bf16(__uint_as_float(u[i]) * inv, __uint_as_float(u[i + 1]) * inv);
+            v.y = pack_bf16(__uint_as_float(u[i + 2]) * inv, __uint_as_float(u[i + 3]) * inv);
+            v.z = pack_bf16(__uint_as_float(u[i + 4]) * inv, __uint_as_float(u[i + 5]) * inv);
+            v.w = pack_bf16(__uint_as_float(u[i + 6]) * inv, __uint_as_float(u[i + 7]) * inv);
+            *reinterpret_cast<uint4*>(orow + 32 * c + i) = v;
+          }
+        }
+      }
+    } else {
+      const int ps = item % a.max_psplits;
+      const int64_t pidx = (static_cast<int64_t>(tok) * a.max_splits + ps) * hq + h;
+      float* o = a.o_part + pidx * kHD;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t u[32];
+        tmem_ld_x32(tmem_o + lane_off + 32 * c, u);
+        tmem_ld_wait();
+        if (row_ok) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(o + 32 * c + i) =
+                make_float4(__uint_as_float(u[i]) * inv, __uint_as_float(u[i + 1]) * inv,
+                            __uint_as_float(u[i + 2]) * inv, __uint_as_float(u[i + 3]) * inv);
+        }
+      }
+      if (row_ok) a.lse_part[pidx] = m_run + log2f(l_run);
+    }
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, kTmemColsTC);
+  }
+}
+
+int32_t launch_fmha(const CUtensorMap* tq, const CUtensorMap* tkv, const FmhaArgs& a, dim3 grid,
+                    cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(fmha_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSmemTC) != cudaSuccess)
+      return CORTEX_ECUDA;
+    configured = true;
+  }
+  fmha_tc_kernel<<<grid, kThreadsTC, kSmemTC, stream>>>(*tq, *tkv, a);
+  CORTEX_CHECK_LAUNCH();
+  return CORTEX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t cortex_fmha_prefill_tc(const void* tmap_kv, const void* tmap_q, void* out,
+                               const int32_t* table, int32_t table_stride, const int32_t* seq_row,
+                               const int32_t* seq_prefix, const int32_t* seq_kvlen,
+                               const int32_t* seq_qstart, const int32_t* seq_qlen, int32_t n_seqs,
+                               int32_t max_qlen, int32_t n_kv_heads, int32_t group,
+                               int64_t k_row0, int64_t v_row0, float softmax_scale,
+                               cudaStream_t stream) {
+  if (!tmap_kv || !tmap_q || !out || !table || n_seqs < 0 || group < 1 || (128 % group) != 0)
+    return CORTEX_EBADARG;
+  if (n_seqs == 0 || max_qlen <= 0) return CORTEX_OK;
+  FmhaArgs a{};
+  a.table = table;
+  a.table_stride = table_stride;
+  a.n_kv_heads = n_kv_heads;
+  a.group = group;
+  a.k_row0 = k_row0;
+  a.v_row0 = v_row0;
+  a.scale_log2 = softmax_scale * kLog2eTC;
+  a.mode = 0;
+  a.seq_row = seq_row;
+  a.seq_prefix = seq_prefix;
+  a.seq_kvlen = seq_kvlen;
+  a.seq_qstart = seq_qstart;
+  a.seq_qlen = seq_qlen;
+  a.out = reinterpret_cast<__nv_bfloat16*>(out);
+  const int tpb = kRows / group;
+  dim3 grid((max_qlen + tpb - 1) / tpb, n_kv_heads, n_seqs);
+  return launch_fmha(reinterpret_cast<const CUtensorMap*>(tmap_q),
+                     reinterpret_cast<const CUtensorMap*>(tmap_kv), a, grid, stream);
+}
+
+int32_t cortex_fmha_cascade_tc(const void* tmap_kv, const void* tmap_q, const int32_t* table,
+                               int32_t table_stride, const int32_t* grp_row,
+                               const int32_t* grp_plen, const int32_t* grp_first,
+                               const int32_t* grp_count, int32_t n_groups, int32_t max_count,
+                               int32_t prefix_slots, int32_t n_kv_heads, int32_t group,
+                               int64_t k_row0, int64_t v_row0, float softmax_scale,
+                               float* o_part, float* lse_part, int32_t max_splits,
+                               cudaStream_t stream) {
+  if (!tmap_kv || !tmap_q || !table || !o_part || !lse_part || n_groups < 0 || group < 1 ||
+      (128 % group) != 0 || prefix_slots < 1)
+    return CORTEX_EBADARG;
+  if (n_groups == 0) return CORTEX_OK;
+  FmhaArgs a{};
+  a.table = table;
+  a.table_stride = table_stride;
+  a.n_kv_heads = n_kv_heads;
+  a.group = group;
+  a.k_row0 = k_row0;
+  a.v_row0 = v_row0;
+  a.scale_log2 = softmax_scale * kLog2eTC;
+  a.mode = 1;
+  a.grp_row = grp_row;
+  a.grp_plen = grp_plen;
+  a.grp_first = grp_first;
+  a.grp_count = grp_count;
+  a.max_psplits = prefix_slots;
+  a.o_part = o_part;
+  a.lse_part = lse_part;
+  a.max_splits = max_splits;
+  const int tpb = kRows / group;
+  dim3 grid((max_count + tpb - 1) / tpb, n_kv_heads, n_groups * prefix_slots);
+  return launch_fmha(reinterpret_cast<const CUtensorMap*>(tmap_q),
+                     reinterpret_cast<const CUtensorMap*>(tmap_kv), a, grid, stream);
+}
+
+}  // extern "C"

@@ -324,6 +324,26 @@ int32_t cortex_tmap_encode_2d_bf16(void* tmap_out, const void* gptr, uint64_t ro
   return r == CUDA_SUCCESS ? CORTEX_OK : CORTEX_ECUDA;
 }
 
+// 3-D bf16 TMA descriptor over q [n_tok, hq, 128] with box (64 dims, group heads,
+// 128/group tokens): 128 query rows (token-major, head-minor) of one GQA group.
+int32_t cortex_tmap_encode_q(void* tmap_out, const void* q, uint64_t n_tok, int32_t hq,
+                             int32_t group) {
+  if (!tmap_out || !q || n_tok == 0 || hq <= 0 || group <= 0 || (128 % group) != 0 ||
+      (reinterpret_cast<uintptr_t>(q) % 16) != 0)
+    return CORTEX_EBADARG;
+  auto fn = get_encode_fn();
+  if (!fn) return CORTEX_ECUDA;
+  cuuint64_t dims[3] = {128, static_cast<cuuint64_t>(hq), n_tok};
+  cuuint64_t strides[2] = {256, static_cast<cuuint64_t>(hq) * 256};
+  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(group), static_cast<cuuint32_t>(128 / group)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(reinterpret_cast<CUtensorMap*>(tmap_out), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                  const_cast<void*>(q), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? CORTEX_OK : CORTEX_ECUDA;
+}
+
 // Split-K factor the GEMM uses for a problem (exported so the host can size the
 // workspace and so tests can pin batch invariance).
 int32_t cortex_gemm_splits(int32_t M, int32_t N, int32_t K) {

@@ -13,6 +13,7 @@ stream per step, every projection a tcgen05 GEMM.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -152,7 +153,9 @@ class GpuWorker:
         self.cos = torch.from_numpy(cos).to(dev)
         self.sin = torch.from_numpy(sin).to(dev)
         # paged KV arena
-        self.cache = torch.empty(cfg.n_layers, 2, n_blocks, cfg.n_kv_heads, BLOCK_TOKENS, HEAD_DIM,
+        # zero-filled once: masked slots of partial blocks are multiplied by p = 0, so the
+        # cache must never hold NaN/Inf bit patterns (stale values are finite)
+        self.cache = torch.zeros(cfg.n_layers, 2, n_blocks, cfg.n_kv_heads, BLOCK_TOKENS, HEAD_DIM,
                                  dtype=BF16, device=dev)
         self.kvmap = ops.kv_map(self.cache.view(-1, HEAD_DIM))
         self.table = torch.zeros(n_rows, row_cols, dtype=torch.int32, device=dev)
@@ -197,6 +200,9 @@ class GpuWorker:
         self.on_forward = None  # optional hook(plan, n_out) for parity checking
         self.prof: KernelProfile | None = None  # optional per-kernel-class CUDA-event timing
         self.cascade = True  # shared-prefix decode attention (prefix KV read once per step)
+        # tcgen05 flash attention for prefill + the cascade pass (CORTEX_TC_ATTN=0: mma.sync)
+        self.tc_attention = os.environ.get("CORTEX_TC_ATTN", "1") != "0"
+        self.qmap = ops.QMap(self.q, cfg.n_heads, cfg.group)
 
     # ------------------------------------------------------------------ helpers
 
@@ -416,15 +422,21 @@ class GpuWorker:
                 e0 = prof.open("attn_decode") if prof is not None else None
                 ops.paged_decode_attn(self.kvmap, self.q, self.table, d_drow, d_dpre, d_dkv, n_dec,
                                       hkv, cfg.group, k0, v0, self.scale, o_part, lse_part,
-                                      max_splits, self.attn, groups=dec_groups)
+                                      max_splits, self.attn, groups=dec_groups,
+                                      qmap=self.qmap if self.tc_attention else None)
                 if e0 is not None:
                     prof.close("attn_decode", e0, dec_bytes, dec_flops)
                 nl += 2
             if n_pf:
                 e0 = prof.open("attn_prefill") if prof is not None else None
-                ops.paged_prefill_attn(self.kvmap, self.q, self.attn, self.table, d_prow, d_ppre,
-                                       d_pkv, d_pqs, d_pql, n_pf, max_qlen, hkv, cfg.group, k0, v0,
-                                       self.scale)
+                if self.tc_attention:
+                    ops.fmha_prefill(self.kvmap, self.qmap, self.attn, self.table, d_prow, d_ppre,
+                                     d_pkv, d_pqs, d_pql, n_pf, max_qlen, hkv, cfg.group, k0, v0,
+                                     self.scale)
+                else:
+                    ops.paged_prefill_attn(self.kvmap, self.q, self.attn, self.table, d_prow,
+                                           d_ppre, d_pkv, d_pqs, d_pql, n_pf, max_qlen, hkv,
+                                           cfg.group, k0, v0, self.scale)
                 if e0 is not None:
                     prof.close("attn_prefill", e0, pf_bytes, pf_flops)
                 nl += 1

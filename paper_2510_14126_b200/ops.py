@@ -164,11 +164,30 @@ def decode_splits(prefix_len: int, kv_len: int) -> int:
     return int(lib().cortex_decode_splits(prefix_len, kv_len))
 
 
+class QMap:
+    """3-D TMA descriptor over q [n_tok, hq, 128] for the tensor-core attention kernels."""
+
+    __slots__ = ("buf", "tensor")
+
+    def __init__(self, q: torch.Tensor, hq: int, group: int) -> None:
+        if q.dtype != torch.bfloat16 or not q.is_contiguous():
+            raise ValueError("QMap needs a contiguous bf16 tensor")
+        self.tensor = q
+        self.buf = ctypes.create_string_buffer(128)
+        n_tok = q.numel() // (hq * 128)
+        _check(lib().cortex_tmap_encode_q(ctypes.addressof(self.buf), q.data_ptr(), n_tok, hq,
+                                          group), "cortex_tmap_encode_q")
+
+    @property
+    def ptr(self) -> int:
+        return ctypes.addressof(self.buf)
+
+
 def paged_decode_attn(kvmap: TensorMap, q, table, seq_row, seq_prefix, seq_kvlen, n_seqs,
                       n_kv_heads, group, k_row0, v_row0, scale, o_part, lse_part, max_splits, out,
-                      groups=None, stream=None) -> None:
+                      groups=None, qmap: QMap | None = None, stream=None) -> None:
     """groups: None, or (grp_row, grp_plen, grp_first, grp_count, n_groups, max_count,
-    prefix_slots) for shared-prefix (cascade) attention."""
+    prefix_slots) for shared-prefix (cascade) attention; qmap selects the tcgen05 cascade."""
     if groups is None:
         g = (None, None, None, None, 0, 0, 0)
     else:
@@ -178,9 +197,23 @@ def paged_decode_attn(kvmap: TensorMap, q, table, seq_row, seq_prefix, seq_kvlen
             kvmap.ptr, q.data_ptr(), table.data_ptr(), table.stride(0), seq_row.data_ptr(),
             seq_prefix.data_ptr(), seq_kvlen.data_ptr(), n_seqs, n_kv_heads, group, k_row0,
             v_row0, scale, o_part.data_ptr(), lse_part.data_ptr(), max_splits, out.data_ptr(),
-            *g, _stream(stream),
+            *g, qmap.ptr if qmap is not None else None, _stream(stream),
         ),
         "cortex_paged_decode_attn",
+    )
+
+
+def fmha_prefill(kvmap: TensorMap, qmap: QMap, out, table, seq_row, seq_prefix, seq_kvlen,
+                 seq_qstart, seq_qlen, n_seqs, max_qlen, n_kv_heads, group, k_row0, v_row0,
+                 scale, stream=None) -> None:
+    _check(
+        lib().cortex_fmha_prefill_tc(
+            kvmap.ptr, qmap.ptr, out.data_ptr(), table.data_ptr(), table.stride(0),
+            seq_row.data_ptr(), seq_prefix.data_ptr(), seq_kvlen.data_ptr(),
+            seq_qstart.data_ptr(), seq_qlen.data_ptr(), n_seqs, max_qlen, n_kv_heads, group,
+            k_row0, v_row0, scale, _stream(stream),
+        ),
+        "cortex_fmha_prefill_tc",
     )
 
 

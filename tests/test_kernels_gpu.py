@@ -201,7 +201,8 @@ def test_paged_decode_attention(cuda, group):
 
 @pytest.mark.parametrize("group", [4, 2])
 @pytest.mark.parametrize("plens", [(1000, 40), (8192,), (16, 5, 0)])
-def test_cascade_decode_attention(cuda, group, plens):
+@pytest.mark.parametrize("impl", ["mma", "tc"])
+def test_cascade_decode_attention(cuda, group, plens, impl):
     """Shared-prefix decode: calls grouped by resident prefix, prefix attended once."""
     o = ops()
     hkv, nb = 2, 2048
@@ -250,7 +251,8 @@ def test_cascade_decode_attention(cuda, group, plens):
     k0, v0 = _rows(0, nb, hkv)
     o.paged_decode_attn(o.kv_map(cache.view(-1, 128)), q, table, dev(seq_row), dev(seq_pre),
                         dev(seq_kv), B, hkv, group, k0, v0, 1 / math.sqrt(128), o_part, lse_part,
-                        max_splits, out, groups=groups)
+                        max_splits, out, groups=groups,
+                        qmap=o.QMap(q, hq, group) if impl == "tc" else None)
     torch.cuda.synchronize()
     for b in range(B):
         k, v = _logical_kv(cache, 0, table[seq_row[b]].cpu(), seq_pre[b], seq_kv[b])
@@ -260,7 +262,8 @@ def test_cascade_decode_attention(cuda, group, plens):
 
 
 @pytest.mark.parametrize("group", [4, 2])
-def test_paged_prefill_attention(cuda, group):
+@pytest.mark.parametrize("impl", ["mma", "tc"])
+def test_paged_prefill_attention(cuda, group, impl):
     o = ops()
     hkv, L, nb, max_blocks = 2, 1, 512, 160
     hq = hkv * group
@@ -280,9 +283,12 @@ def test_paged_prefill_attention(cuda, group):
     kvmap = o.kv_map(cache.view(-1, 128))
     k0, v0 = _rows(0, nb, hkv)
     dev = lambda a: torch.as_tensor(np.asarray(a, dtype=np.int32), device=cuda)
-    o.paged_prefill_attn(kvmap, q, out, table, dev(range(B)), dev([s[0] for s in specs]),
-                         dev([s[1] for s in specs]), dev(qstart), dev(qlens), B, max(qlens), hkv,
-                         group, k0, v0, 1 / math.sqrt(128))
+    args = (table, dev(range(B)), dev([s[0] for s in specs]), dev([s[1] for s in specs]),
+            dev(qstart), dev(qlens), B, max(qlens), hkv, group, k0, v0, 1 / math.sqrt(128))
+    if impl == "mma":
+        o.paged_prefill_attn(kvmap, q, out, *args)
+    else:
+        o.fmha_prefill(kvmap, o.QMap(q, hq, group), out, *args)
     torch.cuda.synchronize()
     for b, (prefix, kvlen) in enumerate(specs):
         k, v = _logical_kv(cache, 0, table[b].cpu(), prefix, kvlen)

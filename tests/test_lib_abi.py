@@ -1,0 +1,46 @@
+"""The C ABI library loads (no GPU needed) and exports every symbol the header declares."""
+
+from __future__ import annotations
+
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def header_symbols() -> list[str]:
+    text = (ROOT / "include" / "cortex_b200.h").read_text()
+    return sorted(set(re.findall(r"^int32_t (cortex_\w+)\(", text, flags=re.M)))
+
+
+def test_header_matches_binding_table():
+    from paper_2510_14126_b200 import _lib
+
+    assert header_symbols() == sorted(_lib.SIGNATURES)
+
+
+def test_library_loads_and_exports_everything():
+    from paper_2510_14126_b200 import _lib
+
+    if not _lib.LIB_PATH.exists():
+        pytest.fail(f"{_lib.LIB_PATH} not built (run python -m paper_2510_14126_b200.build)")
+    lib = _lib.load()
+    for name in header_symbols():
+        assert hasattr(lib, name), name
+    assert lib.cortex_abi_version() == 100
+    # pure host helpers are callable without a GPU
+    assert lib.cortex_gemm_splits(32, 6144, 4096) >= 1
+    assert lib.cortex_decode_splits(1000, 1300) == 6
+    assert lib.cortex_gemm_path(700, 4096, 4096) == 2
+    assert lib.cortex_gemm_path(64, 4096, 4096) == 1
+
+
+def test_no_cpu_fallback_without_library(monkeypatch, tmp_path):
+    from paper_2510_14126_b200 import _lib
+
+    monkeypatch.setattr(_lib, "LIB_PATH", tmp_path / "missing.so")
+    monkeypatch.setattr(_lib, "_LIB", None)
+    with pytest.raises(ImportError):
+        _lib.load()
