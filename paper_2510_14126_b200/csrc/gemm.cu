@@ -215,17 +215,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     if (*last_flag) {
       __threadfence();
-      for (int r = r0; r < rows; r += 4) {
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int z = 0; z < args.splits; ++z) {
-          const float4 v = __ldcg(reinterpret_cast<const float4*>(
-              args.workspace + (static_cast<size_t>(z) * args.M + m0 + r) * args.N + col));
-          acc.x += v.x;
-          acc.y += v.y;
-          acc.z += v.z;
-          acc.w += v.w;
+      for (int rb = r0; rb < rows; rb += 32) {
+        float4 acc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int z = 0; z < args.splits; ++z) {  // split order: deterministic sum
+          const float* wz = args.workspace + static_cast<size_t>(z) * args.M * args.N;
+          float4 v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {  // 8 independent loads in flight
+            const int r = rb + 4 * q;
+            if (r < rows)
+              v[q] = __ldcg(reinterpret_cast<const float4*>(
+                  wz + static_cast<size_t>(m0 + r) * args.N + col));
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            if (rb + 4 * q < rows) {
+              acc[q].x += v[q].x;
+              acc[q].y += v[q].y;
+              acc[q].z += v[q].z;
+              acc[q].w += v[q].w;
+            }
+          }
         }
-        reinterpret_cast<float4*>(stile + r * kBlockN)[lane] = acc;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int r = rb + 4 * q;
+          if (r < rows) reinterpret_cast<float4*>(stile + r * kBlockN)[lane] = acc[q];
+        }
       }
       __syncwarp();
       epilogue_rows(args, stile, m0, rows, r0, lane, col);
@@ -276,7 +294,9 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 
 int32_t cortex_gemm_2sm_launch(const void* tmap_w, const void* tmap_x, int32_t M, int32_t N,
                                int32_t K, void* out, int32_t ldo, int32_t out_f32,
-                               const void* residual, int32_t ldr, cudaStream_t stream);
+                               const void* residual, int32_t ldr, float* workspace,
+                               uint64_t workspace_bytes, int32_t* counters, int32_t n_counters,
+                               cudaStream_t stream);
 
 namespace {
 int g_gemm_mode = 0;  // 0 auto, 1 force the 1-SM (split-K) kernel, 2 force 2-SM when legal
@@ -351,7 +371,7 @@ int32_t cortex_gemm_splits(int32_t M, int32_t N, int32_t K) {
   const int n_tiles = N / kBlockN;
   const int total_kb = K / kBlockK;
   if (M > 256) return 1;
-  const int target = 2 * 148;
+  const int target = 148;  // one wave of 1-CTA-per-SM deep pipelines
   int splits = (target + n_tiles - 1) / n_tiles;
   splits = std::min(splits, std::max(1, total_kb / 4));
   splits = std::min(splits, 16);
@@ -374,7 +394,7 @@ int32_t cortex_gemm_bf16(const void* tmap_w, const void* tmap_x, int32_t M, int3
     return CORTEX_EBADARG;
   if (cortex_gemm_path(M, N, K) == 2)
     return cortex_gemm_2sm_launch(tmap_w, tmap_x, M, N, K, out, ldo, out_f32, residual, ldr,
-                                  stream);
+                                  workspace, workspace_bytes, counters, n_counters, stream);
   GemmArgs a{};
   a.M = M;
   a.N = N;
@@ -408,8 +428,8 @@ int32_t cortex_gemm_bf16(const void* tmap_w, const void* tmap_x, int32_t M, int3
   a.evict_first_w = m_tiles == 1 ? 1 : 0;
   dim3 grid(n_tiles, m_tiles, splits);
   switch (tn) {
-    case 32: return launch_gemm<32, 4>(tw, tx, a, grid, stream);
-    case 64: return launch_gemm<64, 4>(tw, tx, a, grid, stream);
+    case 32: return launch_gemm<32, 8>(tw, tx, a, grid, stream);
+    case 64: return launch_gemm<64, 7>(tw, tx, a, grid, stream);
     case 128: return launch_gemm<128, 5>(tw, tx, a, grid, stream);
     default: return launch_gemm<256, 4>(tw, tx, a, grid, stream);
   }

@@ -22,6 +22,10 @@ constexpr int kBK = 64;
 constexpr int kXBox2 = 16;   // activation rows per TMA box
 constexpr int kEpiRows = 32; // output rows (m) per epilogue chunk
 constexpr int kThreads2 = 192;
+// K splits for the compute-bound GEMM: the deterministic fix-up (partials through L2 + a
+// last-unit reduction) cost more than the wave-quantization it removes at the measured
+// shapes (M=700, N=4096: 70 us split vs 37 us unsplit), so it is off.
+constexpr int kMaxSplits2 = 1;
 
 struct Gemm2Args {
   int M, N, K;
@@ -32,6 +36,10 @@ struct Gemm2Args {
   int ldr;
   int m_tiles;
   int num_tiles;
+  int splits;        // K splits per tile (work units = num_tiles * splits)
+  int kb_per_split;
+  float* workspace;  // [splits][M][N] fp32 partials (splits > 1)
+  int* counters;     // [num_tiles * 2] arrival counters, left zeroed
 };
 
 template <int TN, int STAGES>
@@ -109,6 +117,44 @@ CORTEX_DEVICE void tmem_dealloc_2sm(uint32_t taddr, uint32_t ncols) {
 
 CORTEX_DEVICE void epi_bar_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
 
+// Rows ew, ew+4, ... < crow of a staged fp32 chunk -> (+ fp32 residual) -> bf16 / fp32 out.
+// Each warp covers one 128-column row with 16-byte accesses; all loads before any store
+// (out may alias the residual).
+CORTEX_DEVICE void store_chunk(const Gemm2Args& args, const float* staging, int mrow0, int crow,
+                               int ew, int lane, int col) {
+  float4 v[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int r = ew + 4 * q;
+    if (r < crow) {
+      v[q] = reinterpret_cast<const float4*>(staging + r * 128)[lane];
+      if (args.residual) {
+        const float4 res = *reinterpret_cast<const float4*>(
+            args.residual + static_cast<size_t>(mrow0 + r) * args.ldr + col);
+        v[q].x += res.x;
+        v[q].y += res.y;
+        v[q].z += res.z;
+        v[q].w += res.w;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int r = ew + 4 * q;
+    if (r < crow) {
+      const size_t off = static_cast<size_t>(mrow0 + r) * args.ldo + col;
+      if (args.out_f32) {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(args.out) + off) = v[q];
+      } else {
+        uint2 packed;
+        packed.x = pack_bf16(v[q].x, v[q].y);
+        packed.y = pack_bf16(v[q].z, v[q].w);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(args.out) + off) = packed;
+      }
+    }
+  }
+}
+
 template <int TN, int STAGES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     gemm_bf16_2sm(const __grid_constant__ CUtensorMap tmap_w,
@@ -155,12 +201,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     if (elect_one()) {
       // ---- TMA producer (both CTAs load their halves) ----
       uint32_t it = 0;
-      for (int t = pair; t < args.num_tiles; t += npairs) {
+      for (int u = pair; u < args.num_tiles * args.splits; u += npairs) {
+        const int t = u / args.splits;
+        const int kb0 = (u % args.splits) * args.kb_per_split;
+        const int kb1 = min(total_kb, kb0 + args.kb_per_split);
         const int n_tile = t / args.m_tiles;
         const int m_tile = t % args.m_tiles;
         const int n0 = n_tile * kPairN + rank * 128;
         const int x0 = m_tile * TN + rank * (TN / 2);
-        for (int kb = 0; kb < total_kb; ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
@@ -184,13 +233,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       // ---- MMA issuer (leader CTA, one thread) ----
       constexpr uint32_t idesc = umma_idesc_bf16(kPairN, TN);
       uint32_t it = 0, tl = 0;
-      for (int t = pair; t < args.num_tiles; t += npairs, ++tl) {
+      for (int u = pair; u < args.num_tiles * args.splits; u += npairs, ++tl) {
+        const int kb0 = (u % args.splits) * args.kb_per_split;
+        const int kb1 = min(total_kb, kb0 + args.kb_per_split);
         const uint32_t b = tl & 1;
         const uint32_t tph = (tl >> 1) & 1;
         mbar_wait(&tempty[b], tph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + b * TN;
-        for (int kb = 0; kb < total_kb; ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&full[s], ph);
@@ -200,7 +251,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)
             umma_bf16_ss_2sm(d, umma_desc_sw128(a_addr + k * 32), umma_desc_sw128(b_addr + k * 32),
-                             idesc, (kb | k) != 0 ? 1u : 0u);
+                             idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           umma_commit_2sm_both(&empty[s]);
         }
         umma_commit_2sm_both(&tfull[b]);
@@ -211,8 +262,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     const int quad = warp & 3;
     const int ew = warp - 2;  // 0..3
     const uint32_t tempty_leader_base = mapa_shared(smem_u32(&tempty[0]), 0);
+    int* last_flag = reinterpret_cast<int*>(tmem_holder + 1);
     uint32_t tl = 0;
-    for (int t = pair; t < args.num_tiles; t += npairs, ++tl) {
+    for (int u = pair; u < args.num_tiles * args.splits; u += npairs, ++tl) {
+      const int t = u / args.splits;
+      const int z = u % args.splits;
       const uint32_t b = tl & 1;
       const uint32_t tph = (tl >> 1) & 1;
       const int n_tile = t / args.m_tiles;
@@ -220,6 +274,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       const int n0 = n_tile * kPairN + rank * 128;
       const int m0 = m_tile * TN;
       const int rows = min(TN, args.M - m0);
+      const int col = n0 + 4 * lane;
       mbar_wait(&tfull[b], tph);
       tc_fence_after();
       const uint32_t taddr = tmem_base + b * TN + (static_cast<uint32_t>(quad * 32) << 16);
@@ -234,44 +289,73 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           staging[(16 + j) * 128 + quad * 32 + lane] = __uint_as_float(r1[j]);
         }
         epi_bar_sync();
-        // rows c0 + ew + 4i of this chunk; lane -> columns 4*lane .. +3
         const int crow = min(kEpiRows, rows - c0);
-        const int col = n0 + 4 * lane;
-        float4 v[8];
+        if (args.splits == 1) {
+          store_chunk(args, staging, m0 + c0, crow, ew, lane, col);
+        } else {
+          float* ws = args.workspace + static_cast<size_t>(z) * args.M * args.N;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int r = ew + 4 * u;
-          if (r < crow) {
-            v[u] = reinterpret_cast<const float4*>(staging + r * 128)[lane];
-            if (args.residual) {
-              const float4 res = *reinterpret_cast<const float4*>(
-                  args.residual + static_cast<size_t>(m0 + c0 + r) * args.ldr + col);
-              v[u].x += res.x;
-              v[u].y += res.y;
-              v[u].z += res.z;
-              v[u].w += res.w;
-            }
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int r = ew + 4 * u;
-          if (r < crow) {
-            const size_t off = static_cast<size_t>(m0 + c0 + r) * args.ldo + col;
-            if (args.out_f32) {
-              *reinterpret_cast<float4*>(reinterpret_cast<float*>(args.out) + off) = v[u];
-            } else {
-              uint2 packed;
-              packed.x = pack_bf16(v[u].x, v[u].y);
-              packed.y = pack_bf16(v[u].z, v[u].w);
-              *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(args.out) + off) = packed;
-            }
+          for (int q = 0; q < 8; ++q) {
+            const int r = ew + 4 * q;
+            if (r < crow)
+              __stcg(reinterpret_cast<float4*>(ws + static_cast<size_t>(m0 + c0 + r) * args.N + col),
+                     reinterpret_cast<const float4*>(staging + r * 128)[lane]);
           }
         }
         epi_bar_sync();
       }
+      // the accumulator is drained: release it to the MMA warp before any fix-up work
       tc_fence_before();
       if (lane == 0) mbar_arrive_cluster(tempty_leader_base + b * 8);
+      if (args.splits > 1) {
+        // last unit of this (tile, CTA half) reduces the partials in split order
+        __threadfence();
+        epi_bar_sync();
+        if (threadIdx.x == 64) {
+          const int prev = atomicAdd(&args.counters[t * 2 + rank], 1);
+          *last_flag = prev == args.splits - 1 ? 1 : 0;
+        }
+        epi_bar_sync();
+        if (*last_flag) {
+          __threadfence();
+          for (int c0 = 0; c0 < rows; c0 += kEpiRows) {
+            const int crow = min(kEpiRows, rows - c0);
+            float4 acc[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int zz = 0; zz < args.splits; ++zz) {  // split order: deterministic sum
+              const float* wz = args.workspace + static_cast<size_t>(zz) * args.M * args.N;
+              float4 v[8];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {  // 8 independent loads in flight
+                const int r = ew + 4 * q;
+                if (r < crow)
+                  v[q] = __ldcg(reinterpret_cast<const float4*>(
+                      wz + static_cast<size_t>(m0 + c0 + r) * args.N + col));
+              }
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                if (ew + 4 * q < crow) {
+                  acc[q].x += v[q].x;
+                  acc[q].y += v[q].y;
+                  acc[q].z += v[q].z;
+                  acc[q].w += v[q].w;
+                }
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int r = ew + 4 * q;
+              if (r < crow) reinterpret_cast<float4*>(staging + r * 128)[lane] = acc[q];
+            }
+            __syncwarp();
+            store_chunk(args, staging, m0 + c0, crow, ew, lane, col);
+            __syncwarp();
+          }
+          if (threadIdx.x == 64) args.counters[t * 2 + rank] = 0;
+        }
+        epi_bar_sync();
+      }
     }
   }
 
@@ -297,7 +381,8 @@ int32_t launch2(const CUtensorMap* tw, const CUtensorMap* tx, const Gemm2Args& a
       return CORTEX_ECUDA;
     configured = true;
   }
-  const int pairs = a.num_tiles < n_sms / 2 ? a.num_tiles : n_sms / 2;
+  const int units = a.num_tiles * a.splits;
+  const int pairs = units < n_sms / 2 ? units : n_sms / 2;
   kern<<<2 * pairs, kThreads2, L::kTotal, stream>>>(*tw, *tx, a);
   CORTEX_CHECK_LAUNCH();
   return CORTEX_OK;
@@ -307,27 +392,33 @@ int g_num_sms = 0;
 
 }  // namespace
 
-// Tile width (m) the 2-SM GEMM uses for a problem: fewest waves x (TN + overhead).
-int cortex_gemm2_tile(int M, int N, int n_sms) {
+// Tile width (m) and K splits the 2-SM GEMM uses for a problem: fewest waves of
+// work units x (per-unit MMA time + overhead), a split costing ~10 % for its fix-up.
+void cortex_gemm2_plan(int M, int N, int K, int n_sms, int* tn_out, int* splits_out) {
   const int n_tiles = N / kPairN;
   const int pairs = n_sms / 2;
-  int best = 256;
-  long best_cost = -1;
+  const int total_kb = K / kBK;
+  double best = -1.0;
   for (int tn : {256, 128, 64}) {
-    const long tiles = static_cast<long>(n_tiles) * ((M + tn - 1) / tn);
-    const long waves = (tiles + pairs - 1) / pairs;
-    const long cost = waves * (tn + 24);
-    if (best_cost < 0 || cost < best_cost) {
-      best_cost = cost;
-      best = tn;
+    for (int sp = 1; sp <= kMaxSplits2; ++sp) {
+      if (sp > 1 && total_kb / sp < 8) break;
+      const long units = static_cast<long>(n_tiles) * ((M + tn - 1) / tn) * sp;
+      const long waves = (units + pairs - 1) / pairs;
+      const double cost = waves * (tn + 24.0) / sp * (sp > 1 ? 1.1 : 1.0);
+      if (best < 0 || cost < best - 1e-9) {
+        best = cost;
+        *tn_out = tn;
+        *splits_out = sp;
+      }
     }
   }
-  return best;
 }
 
 int32_t cortex_gemm_2sm_launch(const void* tmap_w, const void* tmap_x, int32_t M, int32_t N,
                                int32_t K, void* out, int32_t ldo, int32_t out_f32,
-                               const void* residual, int32_t ldr, cudaStream_t stream) {
+                               const void* residual, int32_t ldr, float* workspace,
+                               uint64_t workspace_bytes, int32_t* counters, int32_t n_counters,
+                               cudaStream_t stream) {
   if (N % kPairN || K % kBK || M <= 0) return CORTEX_EBADARG;
   if (g_num_sms == 0) {
     int dev = 0;
@@ -335,7 +426,14 @@ int32_t cortex_gemm_2sm_launch(const void* tmap_w, const void* tmap_x, int32_t M
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms < 2) g_num_sms = 148;
   }
-  const int tn = cortex_gemm2_tile(M, N, g_num_sms);
+  int tn = 256, splits = 1;
+  cortex_gemm2_plan(M, N, K, g_num_sms, &tn, &splits);
+  const int m_tiles = (M + tn - 1) / tn;
+  const int num_tiles = (N / kPairN) * m_tiles;
+  if (splits > 1 && (!workspace || !counters ||
+                     workspace_bytes < static_cast<uint64_t>(splits) * M * N * sizeof(float) ||
+                     n_counters < 2 * num_tiles))
+    splits = 1;
   Gemm2Args a{};
   a.M = M;
   a.N = N;
@@ -345,8 +443,12 @@ int32_t cortex_gemm_2sm_launch(const void* tmap_w, const void* tmap_x, int32_t M
   a.out_f32 = out_f32;
   a.residual = reinterpret_cast<const float*>(residual);
   a.ldr = ldr;
-  a.m_tiles = (M + tn - 1) / tn;
-  a.num_tiles = (N / kPairN) * a.m_tiles;
+  a.m_tiles = m_tiles;
+  a.num_tiles = num_tiles;
+  a.splits = splits;
+  a.kb_per_split = (K / kBK + splits - 1) / splits;
+  a.workspace = workspace;
+  a.counters = counters;
   const auto* tw = reinterpret_cast<const CUtensorMap*>(tmap_w);
   const auto* tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
   switch (tn) {
