@@ -39,8 +39,7 @@ constexpr int kPBytes = kRows * 128 * 2;                 // 32 KiB
 constexpr int kStagesTC = 2;
 constexpr int kOffQ = 0;
 constexpr int kOffKV = kQBytes;
-constexpr int kOffP = kOffKV + kStagesTC * kKVStage;
-constexpr int kOffBar = kOffP + 2 * kPBytes;  // P hi, P lo
+constexpr int kOffBar = kOffKV + kStagesTC * kKVStage;
 constexpr int kSmemTC = kOffBar + 256 + 1024;
 constexpr uint32_t kTmemColsTC = 512;  // S0 [0,128) S1 [128,256) O [256,384)
 
@@ -86,6 +85,28 @@ CORTEX_DEVICE BlockRef block_ref(const int* table_row, int prefix_len, int kv_le
   }
   r.block = __ldg(&table_row[j]);
   if (j < npb) {
+    r.pos0 = j * kBlk;
+    r.nvalid = min(kBlk, prefix_len - j * kBlk);
+  } else {
+    const int jj = j - npb;
+    r.pos0 = prefix_len + jj * kBlk;
+    r.nvalid = min(kBlk, kv_len - prefix_len - jj * kBlk);
+  }
+  return r;
+}
+
+struct BlockSpan {
+  int pos0, nvalid;
+};
+
+// Positions of block j of a row (no table access): prefix blocks first, then private.
+CORTEX_DEVICE BlockSpan block_span(int prefix_len, int kv_len, int j, int blk_end) {
+  BlockSpan r;
+  const int npb = (prefix_len + kBlk - 1) / kBlk;
+  if (j >= blk_end) {
+    r.pos0 = 0;
+    r.nvalid = 0;
+  } else if (j < npb) {
     r.pos0 = j * kBlk;
     r.nvalid = min(kBlk, prefix_len - j * kBlk);
   } else {
@@ -144,6 +165,17 @@ CORTEX_DEVICE void tmem_st_x32(uint32_t taddr, const uint32_t (&r)[32]) {
       : "memory");
 }
 
+// D[tmem] (+)= A[tmem] . B[smem]  (A = 128 rows x 16 K, bf16 packed 2 per column)
+CORTEX_DEVICE void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t desc_b, uint32_t idesc,
+                                uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(desc_b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 CORTEX_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
 // mbarrier wait that traps (with a diagnostic) instead of hanging forever when a
@@ -181,13 +213,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
   uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;    // [2]
-  uint64_t* p_full = bars + 7;
-  uint64_t* p_empty = bars + 8;
-  uint64_t* o_done = bars + 9;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* k_full = bars + 1;    // [2]  K and V rings are separate: K of tile t+2 can
+  uint64_t* k_empty = bars + 3;   // [2]  stream in as soon as S_t is done, V as soon as
+  uint64_t* v_full = bars + 5;    // [2]  PV_t is done
+  uint64_t* v_empty = bars + 7;   // [2]
+  uint64_t* s_full = bars + 9;    // [2]
+  uint64_t* p_full = bars + 11;
+  uint64_t* o_ready = bars + 12;  // committed after every PV (O stable for a rescale)
+  uint64_t* o_done = bars + 13;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 14);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -237,12 +271,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     tma_prefetch_desc(&tmap_kv);
     mbar_init(q_full, 1);
     for (int s = 0; s < kStagesTC; ++s) {
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
       mbar_init(&s_full[s], 1);
     }
     mbar_init(p_full, 4);
-    mbar_init(p_empty, 1);
+    mbar_init(o_ready, 1);
     mbar_init(o_done, 1);
     fence_mbar_init();
   }
@@ -263,18 +299,29 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       for (int kt = 0; kt < n_kt; ++kt) {
         const int s = kt % kStagesTC;
         const uint32_t ph = (kt / kStagesTC) & 1;
-        mbar_wait_guard(&kv_empty[s], ph ^ 1);
         uint8_t* st = smem + kOffKV + s * kKVStage;
-        mbar_arrive_expect_tx(&kv_full[s], kKVStage);
+        int rows[kBlocksPerTile];
+#pragma unroll
         for (int j = 0; j < kBlocksPerTile; ++j) {
           const BlockRef b = block_ref(table_row, prefix_len, kv_len,
                                        blk_begin + kt * kBlocksPerTile + j, blk_end);
-          const int64_t r = (static_cast<int64_t>(b.block) * a.n_kv_heads + kvh) * kBlk;
+          rows[j] = static_cast<int>((static_cast<int64_t>(b.block) * a.n_kv_heads + kvh) * kBlk);
+        }
+        mbar_wait_guard(&k_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&k_full[s], 2 * kKVHalf);
+#pragma unroll
+        for (int j = 0; j < kBlocksPerTile; ++j) {
           const int off = j * kBlk * 128;
-          tma_load_2d(st + 0 * kKVHalf + off, &tmap_kv, &kv_full[s], 0, static_cast<int>(a.k_row0 + r));
-          tma_load_2d(st + 1 * kKVHalf + off, &tmap_kv, &kv_full[s], 64, static_cast<int>(a.k_row0 + r));
-          tma_load_2d(st + 2 * kKVHalf + off, &tmap_kv, &kv_full[s], 0, static_cast<int>(a.v_row0 + r));
-          tma_load_2d(st + 3 * kKVHalf + off, &tmap_kv, &kv_full[s], 64, static_cast<int>(a.v_row0 + r));
+          tma_load_2d(st + 0 * kKVHalf + off, &tmap_kv, &k_full[s], 0, static_cast<int>(a.k_row0) + rows[j]);
+          tma_load_2d(st + 1 * kKVHalf + off, &tmap_kv, &k_full[s], 64, static_cast<int>(a.k_row0) + rows[j]);
+        }
+        mbar_wait_guard(&v_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&v_full[s], 2 * kKVHalf);
+#pragma unroll
+        for (int j = 0; j < kBlocksPerTile; ++j) {
+          const int off = j * kBlk * 128;
+          tma_load_2d(st + 2 * kKVHalf + off, &tmap_kv, &v_full[s], 0, static_cast<int>(a.v_row0) + rows[j]);
+          tma_load_2d(st + 3 * kKVHalf + off, &tmap_kv, &v_full[s], 64, static_cast<int>(a.v_row0) + rows[j]);
         }
       }
     }
@@ -284,13 +331,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128);
       constexpr uint32_t idesc_pv = umma_idesc_bf16(128, 128) | (1u << 16);  // B (V) MN-major
       const uint32_t q_addr = smem_u32(smem + kOffQ);
-      const uint32_t p_addr = smem_u32(smem + kOffP);
       mbar_wait_guard(q_full, 0);
       for (int kt = 0; kt <= n_kt; ++kt) {
         if (kt < n_kt) {
           const int s = kt % kStagesTC;
           const uint32_t ph = (kt / kStagesTC) & 1;
-          mbar_wait_guard(&kv_full[s], ph);
+          mbar_wait_guard(&k_full[s], ph);
           tc_fence_after();
           const uint32_t k_addr = smem_u32(smem + kOffKV + s * kKVStage);
 #pragma unroll
@@ -299,28 +345,30 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             umma_bf16_ss(tmem_s + 128 * s, umma_desc_sw128(q_addr + off),
                          umma_desc_sw128(k_addr + off), idesc_s, kk != 0 ? 1u : 0u);
           }
+          umma_commit(&k_empty[s]);
           umma_commit(&s_full[s]);
         }
         if (kt > 0) {
           const int t = kt - 1;
           const int s = t % kStagesTC;
+          mbar_wait_guard(&v_full[s], (t / kStagesTC) & 1);
           mbar_wait_guard(p_full, t & 1);
           tc_fence_after();
           const uint32_t v_addr = smem_u32(smem + kOffKV + s * kKVStage + 2 * kKVHalf);
-          // O += P_hi V + P_lo V  (P = P_hi + P_lo to ~2^-17)
+          // O += P_hi V + P_lo V  (P = P_hi + P_lo to ~2^-17); P lives in TMEM over the
+          // S buffer it was computed from (A operand from TMEM, 8 columns per 16 keys)
+          const uint32_t p_tmem = tmem_s + 128 * s;
 #pragma unroll
           for (int part = 0; part < 2; ++part) {
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
-              umma_bf16_ss(tmem_o,
-                           umma_desc_sw128(p_addr + part * kPBytes + (kk >> 2) * kKVHalf +
-                                           (kk & 3) * 32),
+              umma_bf16_ts(tmem_o, p_tmem + 64 * part + 8 * kk,
                            umma_desc_sw128_mn(v_addr + kk * 2048, kKVHalf), idesc_pv,
                            (t | kk | part) != 0 ? 1u : 0u);
             }
           }
-          umma_commit(&kv_empty[s]);
-          umma_commit(p_empty);
+          umma_commit(&v_empty[s]);
+          umma_commit(o_ready);
           if (t == n_kt - 1) umma_commit(o_done);
         }
       }
@@ -333,7 +381,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const bool row_ok = r < ntok * group;
     const int qpos = qpos_base + r / group;
     float m_run = -INFINITY, l_run = 0.f;
-    uint8_t* psm = smem + kOffP;
     for (int kt = 0; kt < n_kt; ++kt) {
       const int s = kt % kStagesTC;
       mbar_wait_guard(&s_full[s], (kt / kStagesTC) & 1);
@@ -347,30 +394,52 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) sv[32 * c + i] = __uint_as_float(u[i]);
       }
-      // mask + tile max
-      float mt = -INFINITY;
+      // tile max (raw scores; scale > 0 commutes with max). Fast path when every key
+      // of the tile is valid and visible to every row of the CTA (CTA-uniform test);
+      // otherwise mask: invalid slots of partial blocks, causal, rows past the end.
+      const int j0 = blk_begin + kt * kBlocksPerTile;
+      bool full = j0 + kBlocksPerTile <= blk_end;
 #pragma unroll
       for (int j = 0; j < kBlocksPerTile; ++j) {
-        const BlockRef b = block_ref(table_row, prefix_len, kv_len,
-                                     blk_begin + kt * kBlocksPerTile + j, blk_end);
+        const BlockSpan b = block_span(prefix_len, kv_len, j0 + j, blk_end);
+        full = full && b.nvalid == kBlk && b.pos0 + kBlk - 1 <= qpos_base;
+      }
+      float mraw = -INFINITY;
+      if (full) {
 #pragma unroll
-        for (int i = 0; i < kBlk; ++i) {
-          const bool ok = row_ok && i < b.nvalid && b.pos0 + i <= qpos;
-          const float v = ok ? sv[kBlk * j + i] * a.scale_log2 : -INFINITY;
-          sv[kBlk * j + i] = v;
-          mt = fmaxf(mt, v);
+        for (int i = 0; i < 128; ++i) mraw = fmaxf(mraw, sv[i]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < kBlocksPerTile; ++j) {
+          const BlockSpan b = block_span(prefix_len, kv_len, j0 + j, blk_end);
+#pragma unroll
+          for (int i = 0; i < kBlk; ++i) {
+            const bool ok = row_ok && i < b.nvalid && b.pos0 + i <= qpos;
+            sv[kBlk * j + i] = ok ? sv[kBlk * j + i] : -INFINITY;
+            mraw = fmaxf(mraw, sv[kBlk * j + i]);
+          }
         }
       }
-      // wait until PV of the previous tile finished (P smem free, O stable)
-      if (kt > 0) mbar_wait_guard(p_empty, (kt - 1) & 1);
-      tc_fence_after();
+      const float mt = mraw * a.scale_log2;  // -inf stays -inf
       // running max: adopt the tile max when the row had none yet (its O row is 0), or
       // when it grew by more than 2^8 (then O and l are rescaled); otherwise keep the
       // stale max (p <= 2^8, exact after the final 1/l).
       const bool adopt = mt > -INFINITY && (m_run == -INFINITY || mt > m_run + kRescaleThresh);
       const float alpha = !adopt ? 1.f : (m_run == -INFINITY ? 0.f : exp2f(m_run - mt));
-      // O rescale (tcgen05.ld/st are warp-collective: decided per warp, alpha per row)
+      const float m_new = adopt ? mt : m_run;
+      const float m_use = m_new == -INFINITY ? 0.f : m_new;
+      // p = exp2(s * scale - m), computed before waiting for the previous PV
+      float lsum = 0.f;
+#pragma unroll
+      for (int i = 0; i < 128; ++i) {
+        sv[i] = exp2f(fmaf(sv[i], a.scale_log2, -m_use));
+        lsum += sv[i];
+      }
+      // O rescale (rare; tcgen05.ld/st are warp-collective: decided per warp, alpha per
+      // row) needs PV of the previous tile finished
       if (kt > 0 && __any_sync(0xffffffffu, adopt && m_run != -INFINITY)) {
+        mbar_wait_guard(o_ready, (kt - 1) & 1);
+        tc_fence_after();
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t u[32];
@@ -382,31 +451,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
         tmem_st_wait();
       }
-      if (adopt) {
-        l_run *= alpha;
-        m_run = mt;
-      }
-      const float m_use = m_run == -INFINITY ? 0.f : m_run;
-      // P = exp2(s - m) -> bf16 row into the swizzled K-major P tile
+      l_run = l_run * alpha + lsum;
+      m_run = m_new;
+      // P (bf16 hi + lo, keys 2c / 2c+1 packed in column c) -> TMEM over this S buffer
 #pragma unroll
-      for (int ch = 0; ch < 16; ++ch) {
-        float p[8];
+      for (int h = 0; h < 2; ++h) {
+        uint32_t hi[32], lo[32];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          p[e] = exp2f(sv[8 * ch + e] - m_use);
-          l_run += p[e];
-        }
-        uint4 hi, lo;
-        split_bf16(p[0], p[1], hi.x, lo.x);
-        split_bf16(p[2], p[3], hi.y, lo.y);
-        split_bf16(p[4], p[5], hi.z, lo.z);
-        split_bf16(p[6], p[7], hi.w, lo.w);
-        const int half = ch >> 3;
-        const uint32_t off = half * kKVHalf + sw128_offset(r, ch & 7);
-        *reinterpret_cast<uint4*>(psm + off) = hi;
-        *reinterpret_cast<uint4*>(psm + kPBytes + off) = lo;
+        for (int c = 0; c < 32; ++c) split_bf16(sv[64 * h + 2 * c], sv[64 * h + 2 * c + 1], hi[c], lo[c]);
+        tmem_st_x32(tmem_s + 128 * s + lane_off + 32 * h, hi);
+        tmem_st_x32(tmem_s + 128 * s + lane_off + 64 + 32 * h, lo);
       }
-      fence_async_smem();
+      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
