@@ -152,6 +152,21 @@ int32_t cortex_paged_decode_attn(const void* tmap_kv, const void* q, const int32
                                  int32_t prefix_slots, const void* tmap_q,
                                  cortex_stream_t stream);
 
+/* Same as cortex_paged_decode_attn, one part at a time (parts bitmask: 1 = shared-prefix
+ * cascade pass, 2 = per-call context splits, 4 = LSE combine), so the cascade pass can run
+ * on a second stream concurrently with the split kernel (join before the combine). */
+int32_t cortex_paged_decode_attn_parts(const void* tmap_kv, const void* q, const int32_t* table,
+                                       int32_t table_stride, const int32_t* seq_row,
+                                       const int32_t* seq_prefix, const int32_t* seq_kvlen,
+                                       int32_t n_seqs, int32_t n_kv_heads, int32_t group,
+                                       int64_t k_row0, int64_t v_row0, float softmax_scale,
+                                       float* o_part, float* lse_part, int32_t max_splits,
+                                       void* out, const int32_t* grp_row, const int32_t* grp_plen,
+                                       const int32_t* grp_first, const int32_t* grp_count,
+                                       int32_t n_groups, int32_t max_group_count,
+                                       int32_t prefix_slots, const void* tmap_q, int32_t parts,
+                                       cortex_stream_t stream);
+
 /* TMA descriptor over q [n_tok, hq, 128] (box 64 dims x group heads x 128/group tokens)
  * for the tensor-core attention kernels; tmap_q above selects the tcgen05 cascade pass. */
 int32_t cortex_tmap_encode_q(void* tmap_out, const void* q, uint64_t n_tok, int32_t hq,

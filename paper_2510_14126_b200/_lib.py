@@ -38,6 +38,8 @@ SIGNATURES: dict[str, list] = {
     "cortex_decode_splits": [I32, I32],
     "cortex_paged_decode_attn": [P, P, P, I32, P, P, P, I32, I32, I32, I64, I64, F32, P, P, I32,
                                  P, P, P, P, P, I32, I32, I32, P, P],
+    "cortex_paged_decode_attn_parts": [P, P, P, I32, P, P, P, I32, I32, I32, I64, I64, F32, P, P,
+                                       I32, P, P, P, P, P, I32, I32, I32, P, I32, P],
     "cortex_tmap_encode_q": [P, P, U64, I32, I32],
     "cortex_fmha_prefill_tc": [P, P, P, P, I32, P, P, P, P, P, I32, I32, I32, I32, I64, I64, F32,
                                P],

@@ -470,10 +470,14 @@ struct CombineArgs {
   int slot_off;
 };
 
-__global__ void __launch_bounds__(kHeadDim) decode_combine_kernel(const CombineArgs a) {
+// LSE merge of a call's partials: one CTA per call, warp <-> head, lane <-> 4 dims;
+// slot weights computed once per head by the lanes, partial rows loaded 4 at a time.
+constexpr int kCombineThreads = 256;
+
+__global__ void __launch_bounds__(kCombineThreads) decode_combine_kernel(const CombineArgs a) {
   const int b = blockIdx.x;
-  const int h = blockIdx.y;
-  const int d = threadIdx.x;
+  const int warp = warp_id();
+  const int lane = lane_id();
   const int prefix = __ldg(&a.seq_prefix[b]);
   const int ntiles = num_tiles(prefix, __ldg(&a.seq_kvlen[b]));
   // slot ranges: [0, np) prefix partials (cascade), [off, off + ns) context splits
@@ -486,24 +490,51 @@ __global__ void __launch_bounds__(kHeadDim) decode_combine_kernel(const CombineA
   } else {
     ns = (ntiles + kTilesPerSplit - 1) / kTilesPerSplit;
   }
+  const int nsl = np + ns;
   const int64_t base = static_cast<int64_t>(b) * a.max_splits;
-  float M = -INFINITY;
-  for (int s = 0; s < np; ++s) M = fmaxf(M, a.lse_part[(base + s) * a.hq + h]);
-  for (int s = off; s < off + ns; ++s) M = fmaxf(M, a.lse_part[(base + s) * a.hq + h]);
-  float L = 0.f, O = 0.f;
-  for (int s = 0; s < np; ++s) {
-    const int64_t pidx = (base + s) * a.hq + h;
-    const float w = exp2f(a.lse_part[pidx] - M);
-    L += w;
-    O += w * a.o_part[pidx * kHeadDim + d];
+  auto slot = [&](int i) { return i < np ? i : off + (i - np); };
+  for (int h = warp; h < a.hq; h += kCombineThreads / 32) {
+    float M = -INFINITY;
+    for (int i = lane; i < nsl; i += 32) M = fmaxf(M, a.lse_part[(base + slot(i)) * a.hq + h]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    float L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i0 = 0; i0 < nsl; i0 += 32) {
+      const int i = i0 + lane;
+      const float w = i < nsl ? exp2f(a.lse_part[(base + slot(i)) * a.hq + h] - M) : 0.f;
+      L += w;
+      const int cnt = min(32, nsl - i0);
+      for (int j = 0; j < cnt; j += 4) {
+        float4 v[4];
+        float wj[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          wj[u] = __shfl_sync(0xffffffffu, w, (j + u) & 31);
+          if (j + u < cnt)
+            v[u] = *reinterpret_cast<const float4*>(
+                a.o_part + ((base + slot(i0 + j + u)) * a.hq + h) * kHeadDim + 4 * lane);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (j + u < cnt) {
+            acc.x += wj[u] * v[u].x;
+            acc.y += wj[u] * v[u].y;
+            acc.z += wj[u] * v[u].z;
+            acc.w += wj[u] * v[u].w;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+    const float inv = 1.f / L;
+    uint2 packed;
+    packed.x = pack_bf16(acc.x * inv, acc.y * inv);
+    packed.y = pack_bf16(acc.z * inv, acc.w * inv);
+    *reinterpret_cast<uint2*>(a.out + (static_cast<int64_t>(b) * a.hq + h) * kHeadDim + 4 * lane) =
+        packed;
   }
-  for (int s = off; s < off + ns; ++s) {
-    const int64_t pidx = (base + s) * a.hq + h;
-    const float w = exp2f(a.lse_part[pidx] - M);
-    L += w;
-    O += w * a.o_part[pidx * kHeadDim + d];
-  }
-  a.out[(static_cast<int64_t>(b) * a.hq + h) * kHeadDim + d] = __float2bfloat16_rn(O / L);
 }
 
 // ---------------------------------------------------------------------------
@@ -648,6 +679,24 @@ int32_t cortex_paged_decode_attn(const void* tmap_kv, const void* q, const int32
                                  const int32_t* grp_first, const int32_t* grp_count,
                                  int32_t n_groups, int32_t max_group_count,
                                  int32_t prefix_slots, const void* tmap_q, cudaStream_t stream) {
+  return cortex_paged_decode_attn_parts(tmap_kv, q, table, table_stride, seq_row, seq_prefix,
+                                        seq_kvlen, n_seqs, n_kv_heads, group, k_row0, v_row0,
+                                        softmax_scale, o_part, lse_part, max_splits, out, grp_row,
+                                        grp_plen, grp_first, grp_count, n_groups, max_group_count,
+                                        prefix_slots, tmap_q, 7, stream);
+}
+
+int32_t cortex_paged_decode_attn_parts(const void* tmap_kv, const void* q, const int32_t* table,
+                                       int32_t table_stride, const int32_t* seq_row,
+                                       const int32_t* seq_prefix, const int32_t* seq_kvlen,
+                                       int32_t n_seqs, int32_t n_kv_heads, int32_t group,
+                                       int64_t k_row0, int64_t v_row0, float softmax_scale,
+                                       float* o_part, float* lse_part, int32_t max_splits,
+                                       void* out, const int32_t* grp_row, const int32_t* grp_plen,
+                                       const int32_t* grp_first, const int32_t* grp_count,
+                                       int32_t n_groups, int32_t max_group_count,
+                                       int32_t prefix_slots, const void* tmap_q, int32_t parts,
+                                       cudaStream_t stream) {
   if (!tmap_kv || !q || !table || !seq_row || !seq_prefix || !seq_kvlen || !o_part ||
       !lse_part || !out || n_seqs < 0 || group < 1 || group > 8 || (16 % group) != 0 ||
       max_splits < 1 || n_groups < 0)
@@ -658,7 +707,9 @@ int32_t cortex_paged_decode_attn(const void* tmap_kv, const void* q, const int32
                   prefix_slots >= max_splits))
     return CORTEX_EBADARG;
   const float scale_log2 = softmax_scale * kLog2e;
-  if (cascade && tmap_q) {
+  if (!(parts & 1)) {
+    // cascade pass launched separately (e.g. on a side stream)
+  } else if (cascade && tmap_q) {
     const int32_t rc = cortex_fmha_cascade_tc(
         tmap_kv, tmap_q, table, table_stride, grp_row, grp_plen, grp_first, grp_count, n_groups,
         max_group_count, prefix_slots, n_kv_heads, group, k_row0, v_row0, softmax_scale, o_part,
@@ -721,10 +772,13 @@ int32_t cortex_paged_decode_attn(const void* tmap_kv, const void* q, const int32
       return CORTEX_ECUDA;
     configured = true;
   }
-  dim3 grid(max_splits - a.slot_off, n_kv_heads, n_seqs);
-  paged_decode_kernel<<<grid, kWarps * 32, smem, stream>>>(
-      *reinterpret_cast<const CUtensorMap*>(tmap_kv), a);
-  CORTEX_CHECK_LAUNCH();
+  if (parts & 2) {
+    dim3 grid(max_splits - a.slot_off, n_kv_heads, n_seqs);
+    paged_decode_kernel<<<grid, kWarps * 32, smem, stream>>>(
+        *reinterpret_cast<const CUtensorMap*>(tmap_kv), a);
+    CORTEX_CHECK_LAUNCH();
+  }
+  if (!(parts & 4)) return CORTEX_OK;
   CombineArgs cb{};
   cb.o_part = o_part;
   cb.lse_part = lse_part;
@@ -735,7 +789,7 @@ int32_t cortex_paged_decode_attn(const void* tmap_kv, const void* q, const int32
   cb.max_splits = max_splits;
   cb.cascade = cascade;
   cb.slot_off = a.slot_off;
-  decode_combine_kernel<<<dim3(n_seqs, cb.hq), kHeadDim, 0, stream>>>(cb);
+  decode_combine_kernel<<<n_seqs, kCombineThreads, 0, stream>>>(cb);
   CORTEX_CHECK_LAUNCH();
   return CORTEX_OK;
 }

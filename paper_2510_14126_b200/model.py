@@ -203,6 +203,10 @@ class GpuWorker:
         # tcgen05 flash attention for prefill + the cascade pass (CORTEX_TC_ATTN=0: mma.sync)
         self.tc_attention = os.environ.get("CORTEX_TC_ATTN", "1") != "0"
         self.qmap = ops.QMap(self.q, cfg.n_heads, cfg.group)
+        self.overlap_cascade = True
+        self.side = torch.cuda.Stream(device=dev)
+        self._ev_fork = torch.cuda.Event()
+        self._ev_join = torch.cuda.Event()
 
     # ------------------------------------------------------------------ helpers
 
@@ -420,10 +424,23 @@ class GpuWorker:
             nl += 3
             if n_dec:
                 e0 = prof.open("attn_decode") if prof is not None else None
-                ops.paged_decode_attn(self.kvmap, self.q, self.table, d_drow, d_dpre, d_dkv, n_dec,
-                                      hkv, cfg.group, k0, v0, self.scale, o_part, lse_part,
-                                      max_splits, self.attn, groups=dec_groups,
-                                      qmap=self.qmap if self.tc_attention else None)
+                dargs = (self.kvmap, self.q, self.table, d_drow, d_dpre, d_dkv, n_dec, hkv,
+                         cfg.group, k0, v0, self.scale, o_part, lse_part, max_splits, self.attn)
+                qmap = self.qmap if self.tc_attention else None
+                if dec_groups is not None and qmap is not None and self.overlap_cascade:
+                    # shared-prefix pass (tensor cores, L2) on a side stream, concurrent with
+                    # the per-call context splits (HBM); join before the LSE combine
+                    main = torch.cuda.current_stream()
+                    self._ev_fork.record(main)
+                    self.side.wait_event(self._ev_fork)
+                    ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=1,
+                                          stream=self.side)
+                    ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=2)
+                    self._ev_join.record(self.side)
+                    main.wait_event(self._ev_join)
+                    ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=4)
+                else:
+                    ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap)
                 if e0 is not None:
                     prof.close("attn_decode", e0, dec_bytes, dec_flops)
                 nl += 2

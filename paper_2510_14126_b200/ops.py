@@ -185,19 +185,21 @@ class QMap:
 
 def paged_decode_attn(kvmap: TensorMap, q, table, seq_row, seq_prefix, seq_kvlen, n_seqs,
                       n_kv_heads, group, k_row0, v_row0, scale, o_part, lse_part, max_splits, out,
-                      groups=None, qmap: QMap | None = None, stream=None) -> None:
+                      groups=None, qmap: QMap | None = None, parts: int = 7,
+                      stream=None) -> None:
     """groups: None, or (grp_row, grp_plen, grp_first, grp_count, n_groups, max_count,
-    prefix_slots) for shared-prefix (cascade) attention; qmap selects the tcgen05 cascade."""
+    prefix_slots) for shared-prefix (cascade) attention; qmap selects the tcgen05 cascade;
+    parts: 1 cascade pass | 2 context splits | 4 combine."""
     if groups is None:
         g = (None, None, None, None, 0, 0, 0)
     else:
         g = (_ptr(groups[0]), _ptr(groups[1]), _ptr(groups[2]), _ptr(groups[3])) + tuple(groups[4:])
     _check(
-        lib().cortex_paged_decode_attn(
+        lib().cortex_paged_decode_attn_parts(
             kvmap.ptr, q.data_ptr(), table.data_ptr(), table.stride(0), seq_row.data_ptr(),
             seq_prefix.data_ptr(), seq_kvlen.data_ptr(), n_seqs, n_kv_heads, group, k_row0,
             v_row0, scale, o_part.data_ptr(), lse_part.data_ptr(), max_splits, out.data_ptr(),
-            *g, qmap.ptr if qmap is not None else None, _stream(stream),
+            *g, qmap.ptr if qmap is not None else None, parts, _stream(stream),
         ),
         "cortex_paged_decode_attn",
     )
