@@ -91,7 +91,10 @@ int32_t cortex_tmap_encode_2d_bf16(void* tmap_out, const void* gptr, uint64_t ro
 
 /* tcgen05/TMEM GEMM: out[m, n] = sum_k X[m, k] W[n, k] (+ residual[m, n], fp32 with row
  * pitch ldr; the residual stream is fp32, so residual GEMMs use out_f32 = 1).
- * tmap_w over W [N, K] with box (128, 64); tmap_x over X [>= M, K] with box (32, 64).
+ * tmap_w over W [N, K] with box (128, 64); tmap_x over X [>= M, K] with box (16, 64).
+ * out_f32: 0 = bf16 out, 1 = fp32 out, 2 = fused SwiGLU: W's rows are interleaved in
+ * blocks of 64 gate rows then 64 matching up rows, and out[m, f] (bf16, N/2 features) =
+ * silu(g) * u with g, u the fp32 accumulators (no residual).
  * workspace / counters are used when cortex_gemm_splits(M, N, K) > 1. */
 int32_t cortex_gemm_splits(int32_t M, int32_t N, int32_t K);
 /* Which kernel serves (M, N, K): 1 = 1-SM swap-AB + split-K (decode sizes),

@@ -20,7 +20,7 @@ summation order:
              qkv = bf16(xn Wqkv^T);  q,k = bf16(rope(q,k));  K/V cache bf16
              a = bf16(softmax(q k^T / sqrt(128)) v)        (causal, fp32)
              h = a Wo^T + h
-             xn = bf16(rmsnorm(h) * w_mlp);  gu = bf16(xn Wgu^T)
+             xn = bf16(rmsnorm(h) * w_mlp);  gu = xn Wgu^T (fp32)
              act = bf16(silu(g) * u);  h = act Wd^T + h
   logits = fp32(bf16(rmsnorm(h) * w_final) Wlm^T);  token = first argmax
 """
@@ -140,7 +140,7 @@ class RefSeq:
             a = attention_ref(q, self.k[li], self.v[li], pos, kpos).reshape(n, hq * HEAD_DIM)
             h = a @ w[p + "wo"].T + h
             xn = rmsnorm_ref(h, w[p + "mlp_norm"], c.eps)
-            gu = bf16(xn @ w[p + "wgu"].T)
+            gu = xn @ w[p + "wgu"].T  # fp32: SwiGLU is fused into the GEMM epilogue
             g, u = gu[:, : c.ffn], gu[:, c.ffn:]
             act = bf16(g / (1.0 + torch.exp(-g)) * u)
             h = act @ w[p + "wd"].T + h

@@ -54,6 +54,17 @@ struct GemmSmem {
 // four rows' loads are issued before any store (out may alias residual).
 CORTEX_DEVICE void epilogue_rows(const GemmArgs& a, const float* stile, int m0, int rows, int r0,
                                  int lane, int col) {
+  if (a.out_f32 == 2) {  // fused SwiGLU: tile rows = 64 gate + 64 up features
+    const int f = (col - 4 * lane) / 2 + 2 * lane;
+    for (int r = r0; r < rows; r += 4) {
+      const float2 g = reinterpret_cast<const float2*>(stile + r * kBlockN)[lane];
+      const float2 u = reinterpret_cast<const float2*>(stile + r * kBlockN + 64)[lane];
+      *reinterpret_cast<uint32_t*>(reinterpret_cast<__nv_bfloat16*>(a.out) +
+                                   static_cast<size_t>(m0 + r) * a.ldo + f) =
+          pack_bf16(g.x / (1.f + __expf(-g.x)) * u.x, g.y / (1.f + __expf(-g.y)) * u.y);
+    }
+    return;
+  }
   for (int rb = r0; rb < rows; rb += 16) {
     float4 v[4];
 #pragma unroll

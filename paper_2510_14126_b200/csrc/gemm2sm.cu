@@ -122,6 +122,21 @@ CORTEX_DEVICE void epi_bar_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memor
 // (out may alias the residual).
 CORTEX_DEVICE void store_chunk(const Gemm2Args& args, const float* staging, int mrow0, int crow,
                                int ew, int lane, int col) {
+  if (args.out_f32 == 2) {  // fused SwiGLU: each CTA's 128 rows = 64 gate + 64 up features
+    const int f = (col - 4 * lane) / 2 + 2 * lane;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int r = ew + 4 * q;
+      if (r < crow) {
+        const float2 g = reinterpret_cast<const float2*>(staging + r * 128)[lane];
+        const float2 u = reinterpret_cast<const float2*>(staging + r * 128 + 64)[lane];
+        *reinterpret_cast<uint32_t*>(reinterpret_cast<__nv_bfloat16*>(args.out) +
+                                     static_cast<size_t>(mrow0 + r) * args.ldo + f) =
+            pack_bf16(g.x / (1.f + __expf(-g.x)) * u.x, g.y / (1.f + __expf(-g.y)) * u.y);
+      }
+    }
+    return;
+  }
   float4 v[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {

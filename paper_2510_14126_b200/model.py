@@ -148,6 +148,11 @@ class GpuWorker:
         self.max_seq_tokens = max_seq_tokens
         dev = self.device
         self.w = weights if weights is not None else init_weights(cfg, dev, seed)
+        # gate/up rows interleaved in blocks of 64 so the gate_up GEMM's epilogue applies
+        # SwiGLU in place (the canonical layout stays available via oracle_weights())
+        for i in range(cfg.n_layers):
+            k = f"layers.{i}.wgu"
+            self.w[k] = ops.interleave_gate_up(self.w[k])
         self.wmap = {k: ops.weight_map(v) for k, v in self.w.items() if v.dim() == 2 and k != "embed"}
         cos, sin = rope_tables(max_seq_tokens + 1, cfg.rope_theta)
         self.cos = torch.from_numpy(cos).to(dev)
@@ -169,7 +174,6 @@ class GpuWorker:
         self.qkv = torch.zeros(T, cfg.qkv_dim, dtype=BF16, device=dev)
         self.q = torch.zeros(T, cfg.n_heads * HEAD_DIM, dtype=BF16, device=dev)
         self.attn = torch.zeros(T, cfg.n_heads * HEAD_DIM, dtype=BF16, device=dev)
-        self.gu = torch.zeros(T, 2 * cfg.ffn, dtype=BF16, device=dev)
         self.act = torch.zeros(T, cfg.ffn, dtype=BF16, device=dev)
         self.xn_out = torch.zeros(max_out, d, dtype=BF16, device=dev)
         self.logits = torch.zeros(max_out, cfg.vocab, dtype=torch.float32, device=dev)
@@ -209,6 +213,14 @@ class GpuWorker:
         self._ev_join = torch.cuda.Event()
 
     # ------------------------------------------------------------------ helpers
+
+    def oracle_weights(self) -> dict:
+        """The weights in the canonical layout (gate rows then up rows) — for the checker."""
+        out = dict(self.w)
+        for i in range(self.cfg.n_layers):
+            k = f"layers.{i}.wgu"
+            out[k] = ops.deinterleave_gate_up(self.w[k])
+        return out
 
     def layer_rows(self, layer: int) -> tuple[int, int]:
         per_plane = self.n_blocks * self.cfg.n_kv_heads * BLOCK_TOKENS
@@ -406,13 +418,15 @@ class GpuWorker:
             pf_bytes = float(pf_kvlen.sum()) * tok_kv_bytes + 2 * 2 * (T - n_dec) * hq * HEAD_DIM
             pf_flops = 4.0 * hq * HEAD_DIM * pf_keys
 
-        def gemm(name, xmap, M, out, residual=None):
+        def gemm(name, xmap, M, out, residual=None, swiglu=False):
             e0 = prof.open("gemm") if prof is not None else None
-            ops.gemm(wm[name], xmap, M, out, ws, residual=residual)
+            ops.gemm(wm[name], xmap, M, out, ws, residual=residual, swiglu=swiglu)
             if e0 is not None:
                 N, K = wm[name].rows, wm[name].cols
                 ob = out.element_size() * (2 if residual is not None else 1)
-                prof.close("gemm", e0, 2.0 * N * K + 2.0 * M * K + ob * M * N, 2.0 * M * N * K)
+                n_out = out.shape[1]
+                prof.close("gemm", e0, 2.0 * N * K + 2.0 * M * K + ob * M * n_out,
+                           2.0 * M * N * K)
 
         for li in range(cfg.n_layers):
             p = f"layers.{li}."
@@ -459,8 +473,7 @@ class GpuWorker:
                 nl += 1
             gemm(p + "wo", self.attn_map, T, x, residual=x)
             ops.rmsnorm(x, w[p + "mlp_norm"], T, xn, cfg.eps)
-            gemm(p + "wgu", self.xn_map, T, self.gu)
-            ops.swiglu(self.gu, T, self.act)
+            gemm(p + "wgu", self.xn_map, T, self.act, swiglu=True)  # SwiGLU in the epilogue
             gemm(p + "wd", self.act_map, T, x, residual=x)
             nl += 5
         if n_out:

@@ -84,6 +84,19 @@ class GemmWorkspace:
         self.counters = torch.zeros(n_counters, dtype=torch.int32, device=device)
 
 
+def interleave_gate_up(w: torch.Tensor) -> torch.Tensor:
+    """[gate rows; up rows] (2F x d) -> blocks of 64 gate rows then the matching 64 up rows."""
+    f2, d = w.shape
+    f = f2 // 2
+    return torch.stack([w[:f].view(f // 64, 64, d), w[f:].view(f // 64, 64, d)], dim=1).reshape(f2, d)
+
+
+def deinterleave_gate_up(w: torch.Tensor) -> torch.Tensor:
+    f2, d = w.shape
+    v = w.view(f2 // 128, 2, 64, d)
+    return torch.cat([v[:, 0].reshape(f2 // 2, d), v[:, 1].reshape(f2 // 2, d)])
+
+
 def gemm_splits(M: int, N: int, K: int) -> int:
     return int(lib().cortex_gemm_splits(M, N, K))
 
@@ -97,12 +110,18 @@ def gemm_set_mode(mode: int) -> None:
 
 
 def gemm(wmap: TensorMap, xmap: TensorMap, M: int, out: torch.Tensor, ws: GemmWorkspace,
-         residual: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-    """out[:M] = X[:M] @ W^T (+ residual). out is bf16 or fp32 [>=M, N] row-major."""
+         residual: torch.Tensor | None = None, swiglu: bool = False, stream=None) -> torch.Tensor:
+    """out[:M] = X[:M] @ W^T (+ residual). out is bf16 or fp32 [>=M, N] row-major.
+    swiglu: W rows interleaved (64 gate, 64 up, ...) and out = silu(g) * u, bf16 [>=M, N/2]."""
     N, K = wmap.rows, wmap.cols
     if xmap.cols != K or M > xmap.rows:
         raise ValueError("gemm shape mismatch")
-    out_f32 = 1 if out.dtype == torch.float32 else 0
+    if swiglu:
+        if out.dtype != torch.bfloat16 or out.shape[1] != N // 2 or residual is not None:
+            raise ValueError("swiglu gemm writes bf16 [M, N/2] without residual")
+        out_f32 = 2
+    else:
+        out_f32 = 1 if out.dtype == torch.float32 else 0
     ldr = residual.stride(0) if residual is not None else 0
     _check(
         lib().cortex_gemm_bf16(

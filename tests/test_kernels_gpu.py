@@ -102,6 +102,30 @@ def test_gemm_paths_match(cuda, mode, M, N, K):
     assert rel(out32, ref + r) < 4e-5  # fp32 accumulation order over K <= 14336
 
 
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("M,F,K", [(7, 768, 256), (300, 768, 256), (700, 14336, 4096),
+                                   (64, 14336, 4096)])
+def test_gemm_fused_swiglu(cuda, mode, M, F, K):
+    """gate_up GEMM with SwiGLU applied to the fp32 accumulators in the epilogue."""
+    o = ops()
+    g = torch.Generator(device=cuda).manual_seed(M + F)
+    x = torch.randn(max(M, 32), K, generator=g, device=cuda).to(torch.bfloat16)
+    w = (torch.randn(2 * F, K, generator=g, device=cuda) * 0.05).to(torch.bfloat16)
+    wi = o.interleave_gate_up(w)
+    assert torch.equal(o.deinterleave_gate_up(wi), w)
+    out = torch.full((M, F), float("nan"), device=cuda, dtype=torch.bfloat16)
+    o.gemm_set_mode(mode)
+    try:
+        o.gemm(o.weight_map(wi), o.act_map(x), M, out, o.GemmWorkspace(cuda), swiglu=True)
+        torch.cuda.synchronize()
+    finally:
+        o.gemm_set_mode(0)
+    gu = x[:M].float() @ w.float().T
+    gg, uu = gu[:, :F], gu[:, F:]
+    ref = gg / (1 + torch.exp(-gg)) * uu
+    assert rel(out, ref) < 4e-3
+
+
 def test_gemm_batch_invariant(cuda):
     """Within the decode regime (M <= 128, the 1-SM kernel, split-K fixed by N and K) a
     row's result does not depend on the other rows of the batch."""

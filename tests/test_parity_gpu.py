@@ -110,7 +110,7 @@ def test_config1_engine_parity(cuda):
     assert n_calls == 131
 
     # tokens + logits vs the CPU decoder oracle (teacher forced)
-    dec = RefDecoder(TINY.to_ref(), worker.w, max_pos=16384 + 64)
+    dec = RefDecoder(TINY.to_ref(), worker.oracle_weights(), max_pos=16384 + 64)
     prefix_seqs = {}
     n_tok = mism = 0
     worst_logit = worst_call = 0.0

@@ -64,7 +64,7 @@ def test_runtime_outcomes_and_tokens(cuda, mode):
         assert not e.batch
         assert e.blocks_in_use == sum(p.n_blocks for p in e.resident.values())
     # every 8th SQL against the oracle decoder
-    dec = RefDecoder(TINY.to_ref(), rt.worker.w, max_pos=2048)
+    dec = RefDecoder(TINY.to_ref(), rt.worker.oracle_weights(), max_pos=2048)
     pre = {}
     mism = n_tok = 0
     for rid, sid, visit, p, toks in results[::8]:
