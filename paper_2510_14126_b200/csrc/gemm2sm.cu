@@ -50,7 +50,7 @@ struct G2 {
   static constexpr int kStaging = kEpiRows * 128 * 4;
   static constexpr int kBar = STAGES * kStage + kStaging;
   static constexpr int kTotal = kBar + 512 + 1024;
-  static constexpr uint32_t kTmemCols = 2 * TN;
+  static constexpr uint32_t kTmemCols = 2 * TN <= 128 ? 128 : (2 * TN <= 256 ? 256 : 512);
 };
 
 CORTEX_DEVICE uint32_t cluster_rank() {
@@ -414,12 +414,12 @@ void cortex_gemm2_plan(int M, int N, int K, int n_sms, int* tn_out, int* splits_
   const int pairs = n_sms / 2;
   const int total_kb = K / kBK;
   double best = -1.0;
-  for (int tn : {256, 128, 64}) {
+  for (int tn : {256, 224, 192, 160, 128, 96, 64}) {
     for (int sp = 1; sp <= kMaxSplits2; ++sp) {
       if (sp > 1 && total_kb / sp < 8) break;
       const long units = static_cast<long>(n_tiles) * ((M + tn - 1) / tn) * sp;
       const long waves = (units + pairs - 1) / pairs;
-      const double cost = waves * (tn + 24.0) / sp * (sp > 1 ? 1.1 : 1.0);
+      const double cost = waves * (tn + 32.0) / sp * (sp > 1 ? 1.1 : 1.0);
       if (best < 0 || cost < best - 1e-9) {
         best = cost;
         *tn_out = tn;
@@ -468,7 +468,11 @@ int32_t cortex_gemm_2sm_launch(const void* tmap_w, const void* tmap_x, int32_t M
   const auto* tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
   switch (tn) {
     case 64: return launch2<64, 8>(tw, tx, a, g_num_sms, stream);
-    case 128: return launch2<128, 6>(tw, tx, a, g_num_sms, stream);
+    case 96: return launch2<96, 8>(tw, tx, a, g_num_sms, stream);
+    case 128: return launch2<128, 7>(tw, tx, a, g_num_sms, stream);
+    case 160: return launch2<160, 7>(tw, tx, a, g_num_sms, stream);
+    case 192: return launch2<192, 6>(tw, tx, a, g_num_sms, stream);
+    case 224: return launch2<224, 6>(tw, tx, a, g_num_sms, stream);
     default: return launch2<256, 5>(tw, tx, a, g_num_sms, stream);
   }
 }
