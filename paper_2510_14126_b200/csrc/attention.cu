@@ -382,9 +382,10 @@ __global__ void __launch_bounds__(kWarps * 32)
   if (s0 >= count) return;
   const int plen = __ldg(&a.grp_plen[gi]);
   const int npb = (plen + kTile - 1) / kTile;
-  const int t_begin = ps * kTilesPerSplit;
+  const int psb = prefix_split_blocks(npb, a.max_psplits);
+  const int t_begin = ps * psb;
   if (t_begin >= npb) return;
-  const int t_end = min(npb, t_begin + kTilesPerSplit);
+  const int t_end = min(npb, t_begin + psb);
   const int ntl = t_end - t_begin;
   const int first = __ldg(&a.grp_first[gi]);
   const int row = __ldg(&a.grp_row[gi]);
@@ -484,7 +485,8 @@ __global__ void __launch_bounds__(kCombineThreads) decode_combine_kernel(const C
   int np = 0, off = 0, ns;
   if (a.cascade) {
     const int npb = (prefix + kTile - 1) / kTile;
-    np = (npb + kTilesPerSplit - 1) / kTilesPerSplit;
+    const int psb = npb ? prefix_split_blocks(npb, a.slot_off) : 1;
+    np = (npb + psb - 1) / psb;
     off = a.slot_off;
     ns = (ntiles - npb + kTilesPerSplit - 1) / kTilesPerSplit;
   } else {

@@ -255,9 +255,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     prefix_len = __ldg(&a.grp_plen[g]);
     kv_len = prefix_len;
     const int npb = (prefix_len + kBlk - 1) / kBlk;
-    blk_begin = ps * 16;  // the decode kernels' 16-block split granularity
+    const int psb = prefix_split_blocks(npb, a.max_psplits);  // same split as the combine
+    blk_begin = ps * psb;
     if (blk_begin >= npb) return;
-    blk_end = min(npb, blk_begin + 16);
+    blk_end = min(npb, blk_begin + psb);
     tok0 = __ldg(&a.grp_first[g]) + qb * tpb;
     ntok = min(tpb, count - qb * tpb);
     qpos_base = 0x3fffffff;  // decode queries follow the whole prefix

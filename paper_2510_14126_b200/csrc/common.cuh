@@ -45,6 +45,13 @@ CORTEX_DEVICE bool elect_one() {
   return pred != 0;
 }
 
+// Shared-prefix (cascade) decode attention splits a prefix of npb blocks into `slots`
+// partial slots of this many blocks each (a multiple of the 8-block key tile).
+__host__ __device__ __forceinline__ int prefix_split_blocks(int npb, int slots) {
+  const int per = (npb + slots - 1) / slots;
+  return (per + 7) / 8 * 8;
+}
+
 // --------------------------------------------------------------------------
 // mbarrier
 

@@ -208,6 +208,7 @@ class GpuWorker:
         self.tc_attention = os.environ.get("CORTEX_TC_ATTN", "1") != "0"
         self.qmap = ops.QMap(self.q, cfg.n_heads, cfg.group)
         self.overlap_cascade = True
+        self.cascade_slots = int(os.environ.get("CORTEX_CASCADE_SLOTS", "2"))
         self.side = torch.cuda.Stream(device=dev)
         self._ev_fork = torch.cuda.Event()
         self._ev_join = torch.cuda.Event()
@@ -384,7 +385,9 @@ class GpuWorker:
                 npb = (dec_prefix + BLOCK_TOKENS - 1) // BLOCK_TOKENS
                 ntl = npb + (dec_kvlen - dec_prefix + BLOCK_TOKENS - 1) // BLOCK_TOKENS
                 priv = int(((ntl - npb + 15) // 16).max())
-                pslots = int(((garr[1] + BLOCK_TOKENS - 1) // BLOCK_TOKENS + 15).max() // 16)
+                # prefix partial slots: up to 4 (each a run of key tiles of the cascade pass)
+                pslots = min(self.cascade_slots,
+                             int(((garr[1] + BLOCK_TOKENS - 1) // BLOCK_TOKENS + 15).max() // 16))
                 max_splits = pslots + priv
                 dec_groups = (d_grow, d_gplen, d_gfirst, d_gcount, len(groups), int(garr[3].max()),
                               pslots)
