@@ -109,7 +109,7 @@ def workload(name: str):
 
 
 def build_runtime(model_name: str, wl_name: str, concurrency: int, device, rank: int, world: int,
-                  max_tokens: int = 4096):
+                  max_tokens: int = 4096, role: str = "both", channel=None):
     from paper_2510_14126_b200.config import MODELS
     from paper_2510_14126_b200.engine import EngineParams, blocks_for
     from paper_2510_14126_b200.model import GpuWorker
@@ -124,14 +124,19 @@ def build_runtime(model_name: str, wl_name: str, concurrency: int, device, rank:
     # token capacity that always admits max_batch calls (prefix counted once per engine)
     cap = P + concurrency * (p_hi + o_hi)
     params = EngineParams(cap, 5000.0, 0.02, 0.1, concurrency)
-    n_eng = 2
+    n_eng = 2 if role == "both" else 1
     bpe = blocks_for(params)
     worker = GpuWorker(cfg, device, n_blocks=n_eng * bpe, n_rows=n_eng * (concurrency + 4),
                        row_cols=(max_seq + 15) // 16 + 2, max_tokens=max_tokens,
                        max_out=2 * concurrency + 64, hist_cols=o_hi + 8,
                        max_seq_tokens=max_seq + 16, seed=0)
+    if role == "both":  # replicas: workflows interleaved by rank
+        rid_offset, rid_stride = rank, world
+    else:  # disjoint pairs: workflows interleaved by pair
+        rid_offset, rid_stride = rank % (world // 2), world // 2
     rt = PoolRuntime(worker, spec, params, mode="isolated", concurrency=concurrency, seed=0,
-                     rid_offset=rank, rid_stride=world, prefill_budget=max_tokens - 512)
+                     rid_offset=rid_offset, rid_stride=rid_stride,
+                     prefill_budget=max_tokens - 512, role=role, channel=channel)
     return rt, cfg, desc
 
 
@@ -153,6 +158,9 @@ def main() -> None:
     ap.add_argument("--concurrency", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=40)
+    ap.add_argument("--placement", default="disjoint", choices=["disjoint", "replicas"],
+                    help="N>1: generator and fixer pools on disjoint GPUs (pairs), or "
+                         "both pools on every GPU")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -181,26 +189,55 @@ def main() -> None:
         return
 
     dist = None
+    # CORTEX_DIST_BACKEND=gloo: functional runs with more ranks than GPUs (ranks share a
+    # device; the handoff is host-only, so no kernel waits on another rank)
+    backend = os.environ.get("CORTEX_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
+    comm_dev = torch.device("cuda", local) if backend == "nccl" else torch.device("cpu")
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
 
     from paper_2510_14126_b200.model import KernelProfile
+    from paper_2510_14126_b200.placement import ROLE_BOTH, ROLE_FIXER, open_pair_channel, role_of
 
-    rt, cfg, desc = build_runtime(args.model, args.workload, args.concurrency, device, rank, world)
+    role, pair, _ = role_of(rank, world) if args.placement == "disjoint" else (ROLE_BOTH, rank, -1)
+    # per-GPU load is fixed as N grows: a disjoint pair (2 GPUs) carries 2x the workflows
+    conc = args.concurrency * (2 if role != ROLE_BOTH else 1)
+    channel = open_pair_channel(dist, rank, world, cap=2 * conc + 64) if role != ROLE_BOTH else None
+    rt, cfg, desc = build_runtime(args.model, args.workload, conc, device, rank, world,
+                                  role=role, channel=channel)
     w = rt.worker
     rt.fill()
-    rt.run_steps(max(3, args.warmup))
+
+    def run_phase(n_steps: int, phase: int) -> None:
+        """The generator side (or a replica) runs n_steps; a fixer rank serves its
+        pair until the generator moves the channel past `phase`."""
+        if role == ROLE_FIXER:
+            while channel.phase == phase:
+                rt.step()
+        else:
+            rt.run_steps(n_steps)
+            if channel is not None:
+                channel.phase = phase + 1
+
+    run_phase(max(3, args.warmup), 0)
+    if dist is not None:
+        dist.barrier()
 
     # kernel-class shares (untimed) -> the dominant kernel for the roofline
     w.prof = KernelProfile(["gemm", "attn_decode", "attn_prefill"])
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
-    rt.run_steps(args.profile_steps)
+    run_phase(args.profile_steps, 1)
     e1.record()
     shares = w.prof.summary()
     prof_ms = e0.elapsed_time(e1)
@@ -223,16 +260,23 @@ def main() -> None:
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record()
     kv_samples = []
-    for _ in range(args.steps):
-        rt.step()
-        kv_samples.append(_kv_snapshot(rt))
+    if role == ROLE_FIXER:
+        while channel.phase == 2:
+            rt.step()
+            kv_samples.append(_kv_snapshot(rt))
+    else:
+        for _ in range(args.steps):
+            rt.step()
+            kv_samples.append(_kv_snapshot(rt))
+        if channel is not None:
+            channel.phase = 3
     ev1.record()
     torch.cuda.synchronize()
     t_wall = time.perf_counter() - t_wall0
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
     if dist is not None:
-        t = torch.tensor([ms, t_wall * 1e3], device=device)
+        t = torch.tensor([ms, t_wall * 1e3], device=comm_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, t_wall = float(t[0]), float(t[1]) / 1e3
     s1 = (rt.stats.completed, rt.stats.failed, rt.stats.decode_tokens, rt.stats.prefill_tokens,
@@ -240,7 +284,8 @@ def main() -> None:
     d = [b - a for a, b in zip(s0, s1)]
     completed, failed, dec_tok, pf_tok, steps, launches, h2d, d2h = d
     if dist is not None:
-        t = torch.tensor([completed, failed, dec_tok, pf_tok], device=device, dtype=torch.float64)
+        t = torch.tensor([completed, failed, dec_tok, pf_tok], device=comm_dev,
+                         dtype=torch.float64)
         dist.all_reduce(t)
         completed, failed, dec_tok, pf_tok = [float(x) for x in t]
     kshare = w.prof.summary().get(dominant, {"launches": 0, "ms": 0.0, "bytes": 0.0, "flops": 0.0})
@@ -280,7 +325,10 @@ def main() -> None:
         "dtype": "bf16",
         "data": "synthetic: seeded NL2SQL trace (reference counter streams), random-init weights",
         "config": {"workload": desc, "model": cfg.name + "-shape", "concurrency": args.concurrency,
-                   "engines": "isolated: 1 generator + 1 fixer engine per GPU",
+                   "engines": "isolated: 1 generator + 1 fixer engine per GPU" if role == ROLE_BOTH
+                   else f"isolated, disjoint placement: GPUs 0..{world // 2 - 1} generator pool, "
+                        f"{world // 2}..{world - 1} fixer pool; {world // 2} pair(s) of "
+                        f"{conc} workflows (host handoff, no collective)",
                    "l2": "inputs larger than L2 (16 GB of weights + KV streamed every step)"},
         "decode_tok_s": dec_tok / secs,
         "prefill_tok_s": pf_tok / secs,
@@ -302,6 +350,9 @@ def main() -> None:
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
+        dist.barrier()
+        if channel is not None:
+            channel.close()
         dist.destroy_process_group()
 
 

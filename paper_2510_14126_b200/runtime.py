@@ -46,6 +46,7 @@ from .engine import (
 )
 from .errors import InternalInvariantViolation
 from .model import DecodeTok, GpuWorker, PrefillSeq, StepPlan
+from .placement import ROLE_BOTH, ROLE_FIXER, ROLE_GENERATOR
 from .workflow import EXECUTOR, FIXER, GENERATOR, Nl2Sql, Workflow
 
 
@@ -159,18 +160,37 @@ class RunStats:
     calls: int = 0
     h2d_bytes: int = 0
     d2h_bytes: int = 0
+    handoffs: int = 0
     latencies: list = field(default_factory=list)
 
 
+class _Done:
+    """Completion marker for host-only workers (CPU tests)."""
+
+    @staticmethod
+    def query() -> bool:
+        return True
+
+
 class PoolRuntime:
-    """Closed-loop NL2SQL serving on one GPU (all engines share its weights)."""
+    """Closed-loop NL2SQL serving on one GPU (all engines share its weights).
+
+    `role` selects the stage pools this GPU serves: "both" (the 1-GPU baseline:
+    generator and fixer engines side by side, partitioned HBM) or one side of a
+    disjoint generator/fixer pair (placement.py), with `channel` the pair's
+    shared-memory handoff rings."""
 
     def __init__(self, worker: GpuWorker, spec: Nl2Sql, params: EngineParams, *,
                  mode: str = "isolated", engines_per_pool: tuple[int, int] = (1, 1),
                  concurrency: int = 256, n_workflows: int | None = None, seed: int = 0,
                  rid_offset: int = 0, rid_stride: int = 1, prefill_budget: int | None = None,
-                 n_prefix_rows: int = 4) -> None:
+                 n_prefix_rows: int = 4, role: str = ROLE_BOTH, channel=None) -> None:
         self.worker = worker
+        self.role = role
+        self.channel = channel
+        if role != ROLE_BOTH and (mode != "isolated" or channel is None):
+            raise ValueError("disjoint placement needs isolated pools and a pair channel")
+        self.remote = 0  # workflows of this pair currently owned by the peer rank
         self.spec = spec
         self.params = params
         self.seed = seed
@@ -180,7 +200,11 @@ class PoolRuntime:
         self.rid_stride = rid_stride
         self.prefill_budget = prefill_budget or max(256, worker.max_tokens - params.max_batch * 2)
         tokens = TokenSource(seed, worker.cfg.vocab)
-        if mode == "isolated":
+        if role == ROLE_GENERATOR:
+            pools = [(f"pool:{GENERATOR}", (GENERATOR,), engines_per_pool[0])]
+        elif role == ROLE_FIXER:
+            pools = [(f"pool:{FIXER}", (FIXER,), engines_per_pool[1])]
+        elif mode == "isolated":
             pools = [(f"pool:{GENERATOR}", (GENERATOR,), engines_per_pool[0]),
                      (f"pool:{FIXER}", (FIXER,), engines_per_pool[1])]
         elif mode == "shared":
@@ -211,8 +235,9 @@ class PoolRuntime:
         self._next_rid_i = 0
         self.stats = RunStats()
         self.t0 = time.perf_counter()
+        self._cuda = torch.device(worker.device).type == "cuda"
         self.result_host = torch.zeros(max(64, 2 * concurrency), worker.hist.shape[1],
-                                       dtype=torch.int32, pin_memory=True)
+                                       dtype=torch.int32, pin_memory=self._cuda)
         self._res_i = 0
         self.on_result = None  # optional hook(call, tokens) when a call's SQL reaches the host
         self.finished: list[Workflow] = []
@@ -223,6 +248,8 @@ class PoolRuntime:
         return time.perf_counter() - self.t0
 
     def _start_workflow(self) -> bool:
+        if self.role == ROLE_FIXER:
+            return False  # workflows of a pair start on its generator rank
         if self.n_workflows is not None and self._next_rid_i >= self.n_workflows:
             return False
         rid = self.rid_offset + self._next_rid_i * self.rid_stride
@@ -233,6 +260,15 @@ class PoolRuntime:
         return True
 
     def _enter(self, wf: Workflow) -> None:
+        if wf.stage != EXECUTOR and wf.stage not in self.stage_pool:
+            if self.role != ROLE_GENERATOR or wf.stage != FIXER:
+                raise InternalInvariantViolation(f"no pool serves stage {wf.stage} on this rank")
+            # the fixer pool lives on the peer rank: hand the workflow across (metadata only)
+            self.channel.to_fixer.push(wf.rid, self.t0 + wf.arrival)
+            del self.workflows[wf.rid]
+            self.remote += 1
+            self.stats.handoffs += 1
+            return
         r = wf.enter()
         if wf.stage == EXECUTOR:
             self._tseq += 1
@@ -253,7 +289,10 @@ class PoolRuntime:
             self.stats.latencies.append(wf.done_time - wf.arrival)
             self.finished.append(wf)
             del self.workflows[wf.rid]
-            self._start_workflow()
+            if self.role == ROLE_FIXER:
+                self.channel.to_generator.push(wf.rid, self.t0 + wf.done_time)
+            else:
+                self._start_workflow()
         else:
             self._enter(wf)
 
@@ -297,8 +336,23 @@ class PoolRuntime:
 
     # ------------------------------------------------------------------ step
 
+    def _poll_peer(self) -> None:
+        if self.role == ROLE_GENERATOR:
+            for _rid, _t in self.channel.to_generator.pop_all():  # finished on the fixer rank
+                self.remote -= 1
+                if len(self.workflows) + self.remote < self.concurrency:
+                    self._start_workflow()
+        elif self.role == ROLE_FIXER:
+            for rid, t in self.channel.to_fixer.pop_all():
+                wf = Workflow(rid, self.spec, self.seed, arrival=t - self.t0)
+                wf.replay_to(FIXER)
+                self.workflows[rid] = wf
+                self._enter(wf)
+
     def step(self) -> None:
         w = self.worker
+        if self.channel is not None:
+            self._poll_peer()
         now = self.now()
         while self.timers and self.timers[0][0] <= now:  # executor visits finishing
             _, _, rid = heapq.heappop(self.timers)
@@ -347,8 +401,11 @@ class PoolRuntime:
         i = self._res_i
         self._res_i = (i + 1) % self.result_host.shape[0]
         self.result_host[i, :n].copy_(w.hist[c.slot, :n], non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
+        if self._cuda:
+            ev = torch.cuda.Event()
+            ev.record()
+        else:
+            ev = _Done
         self.stats.d2h_bytes += 4 * n
         e.finish(c)
         self.waiting_d2h.append((ev, c, i, n))
@@ -356,7 +413,7 @@ class PoolRuntime:
     # ------------------------------------------------------------------ driving
 
     def fill(self) -> None:
-        while len(self.workflows) < self.concurrency and self._start_workflow():
+        while len(self.workflows) + self.remote < self.concurrency and self._start_workflow():
             pass
 
     def run_steps(self, k: int) -> None:
@@ -366,7 +423,7 @@ class PoolRuntime:
     def run_until(self, n_completed: int, max_seconds: float = 600.0) -> None:
         t_end = time.perf_counter() + max_seconds
         while self.stats.completed + self.stats.failed < n_completed:
-            if not self.workflows:
+            if not self.workflows and not self.remote and self.role != ROLE_FIXER:
                 break
             self.step()
             if time.perf_counter() > t_end:

@@ -142,6 +142,26 @@ class FakeWorker:
         self.log.append(("first", src, dst))
 
 
+class HostWorker(FakeWorker):
+    """FakeWorker that PoolRuntime can drive: a step is recorded, not computed."""
+
+    def __init__(self, n_blocks: int, n_rows: int, vocab: int = 1024, hist_cols: int = 160,
+                 max_tokens: int = 4096) -> None:
+        import types
+
+        import torch
+
+        super().__init__(n_blocks, n_rows)
+        self.cfg = types.SimpleNamespace(vocab=vocab)
+        self.max_tokens = max_tokens
+        self.hist = torch.zeros(n_rows, hist_cols, dtype=torch.int32)
+        self.steps = 0
+
+    def forward(self, plan) -> int:
+        self.steps += 1
+        return len(plan.decode) + sum(len(s.tokens) for s in plan.prefill)
+
+
 def config1_engines(worker, observer=None, seed: int = 0, vocab: int = 1024):
     params = CONFIG1_PARAMS
     bpe = blocks_for(params)
