@@ -63,6 +63,7 @@ class WallClockEngine(GpuEngineState):
     def __init__(self, *a, **kw) -> None:
         super().__init__(*a, **kw)
         self.pending: deque[_PendingPrefill] = deque()
+        self.cold_admits = 0  # stage-prefix prefills (an admit that found no resident prefix)
 
     def _gpu_admit(self, call: InFlightCall, prefix, cold: bool) -> None:
         w = self.worker
@@ -73,6 +74,7 @@ class WallClockEngine(GpuEngineState):
                 raise InternalInvariantViolation(f"engine {self.engine_id}: no free prefix row")
             prefix.row = self._free_prefix_rows.pop(0)
             prefix.n_blocks = npb
+            self.cold_admits += 1
         call.slot = self._free_slots.pop(0)
         call.prefix_len = P
         call.visit, toks = self.gpu.tokens.prompt(call.request_id, call.stage_id, call.prompt_tokens)
