@@ -133,7 +133,7 @@ int32_t cortex_argmax(const float* logits, int64_t ld, int32_t n_rows, int32_t v
                       int32_t hist_stride, const int32_t* hist_pos, cortex_stream_t stream);
 
 /* Paged decode attention (one query token per sequence), split along the
- * context in fixed 256-token chunks + LSE combine. o_part/lse_part:
+ * context in fixed 512-token chunks + LSE combine. o_part/lse_part:
  * [n_seqs, max_splits, Hq, 128] / [n_seqs, max_splits, Hq] fp32 workspace.
  * Without groups (n_groups = 0): max_splits >= max cortex_decode_splits(prefix, kv_len).
  * Cascade (n_groups > 0): the decode calls sharing a resident stage prefix are
@@ -169,6 +169,25 @@ int32_t cortex_paged_decode_attn_parts(const void* tmap_kv, const void* q, const
                                        int32_t n_groups, int32_t max_group_count,
                                        int32_t prefix_slots, const void* tmap_q, int32_t parts,
                                        cortex_stream_t stream);
+
+/* Balanced ("flat") plan for the context splits: call b's tiles (its private tiles
+ * under cascade, all tiles otherwise) are flat tiles [seq_tile_start[b],
+ * seq_tile_start[b] + n_b) of one sequence of total_tiles; CTA (c, kv head) streams
+ * flat tiles [c W, (c+1) W), W = tiles_per_chunk <= 48 (cortex_decode_tiles_per_chunk),
+ * so every CTA does equal work whatever the context lengths. Call b's partials go to
+ * slots off + [0, (S_b + n_b - 1) / W - S_b / W], off = prefix_slots under cascade
+ * else 0: max_splits must cover that. Other arguments and parts as above; with
+ * seq_tile_start = NULL this is cortex_paged_decode_attn_parts. */
+int32_t cortex_decode_tiles_per_chunk(int32_t total_tiles, int32_t n_kv_heads);
+int32_t cortex_paged_decode_attn_flat(
+    const void* tmap_kv, const void* q, const int32_t* table, int32_t table_stride,
+    const int32_t* seq_row, const int32_t* seq_prefix, const int32_t* seq_kvlen,
+    const int32_t* seq_tile_start, int32_t total_tiles, int32_t tiles_per_chunk, int32_t n_seqs,
+    int32_t n_kv_heads, int32_t group, int64_t k_row0, int64_t v_row0, float softmax_scale,
+    float* o_part, float* lse_part, int32_t max_splits, void* out, const int32_t* grp_row,
+    const int32_t* grp_plen, const int32_t* grp_first, const int32_t* grp_count, int32_t n_groups,
+    int32_t max_group_count, int32_t prefix_slots, const void* tmap_q, int32_t parts,
+    cortex_stream_t stream);
 
 /* TMA descriptor over q [n_tok, hq, 128] (box 64 dims x group heads x 128/group tokens)
  * for the tensor-core attention kernels; tmap_q above selects the tcgen05 cascade pass. */

@@ -7,6 +7,7 @@ of any op fails with an ImportError naming the build command.
 from __future__ import annotations
 
 import ctypes
+import os
 from ctypes import c_float, c_int32, c_int64, c_uint64, c_void_p
 from pathlib import Path
 
@@ -40,6 +41,9 @@ SIGNATURES: dict[str, list] = {
                                  P, P, P, P, P, I32, I32, I32, P, P],
     "cortex_paged_decode_attn_parts": [P, P, P, I32, P, P, P, I32, I32, I32, I64, I64, F32, P, P,
                                        I32, P, P, P, P, P, I32, I32, I32, P, I32, P],
+    "cortex_decode_tiles_per_chunk": [I32, I32],
+    "cortex_paged_decode_attn_flat": [P, P, P, I32, P, P, P, P, I32, I32, I32, I32, I32, I64, I64,
+                                      F32, P, P, I32, P, P, P, P, P, I32, I32, I32, P, I32, P],
     "cortex_tmap_encode_q": [P, P, U64, I32, I32],
     "cortex_fmha_prefill_tc": [P, P, P, P, I32, P, P, P, P, P, I32, I32, I32, I32, I64, I64, F32,
                                P],
@@ -59,12 +63,14 @@ def load() -> ctypes.CDLL:
     """Load the library (once) and declare every export's signature."""
     global _LIB
     if _LIB is None:
-        if not LIB_PATH.exists():
+        # CORTEX_LIB: an alternative build of the same library (tuning variants)
+        path = Path(os.environ.get("CORTEX_LIB", str(LIB_PATH)))
+        if not path.exists():
             raise ImportError(
-                f"{LIB_PATH} is missing; build it with `python -m paper_2510_14126_b200.build` "
+                f"{path} is missing; build it with `python -m paper_2510_14126_b200.build` "
                 "(there is no CPU fallback)"
             )
-        lib = ctypes.CDLL(str(LIB_PATH))
+        lib = ctypes.CDLL(str(path))
         for name, argtypes in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.argtypes = argtypes

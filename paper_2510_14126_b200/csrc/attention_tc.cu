@@ -35,7 +35,6 @@ constexpr float kRescaleThresh = 8.0f;  // log2 units
 constexpr int kQBytes = kRows * kHD * 2;                 // 32 KiB
 constexpr int kKVHalf = kBlocksPerTile * kBlk * 64 * 2;  // 16 KiB  [128 keys x 64 dims]
 constexpr int kKVStage = 4 * kKVHalf;                    // K lo, K hi, V lo, V hi
-constexpr int kPBytes = kRows * 128 * 2;                 // 32 KiB
 constexpr int kStagesTC = 2;
 constexpr int kOffQ = 0;
 constexpr int kOffKV = kQBytes;
@@ -199,10 +198,6 @@ CORTEX_DEVICE void mbar_wait_guard(uint64_t* bar, uint32_t parity) {
       __trap();
     }
   }
-}
-
-CORTEX_DEVICE void fence_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
 __global__ void __launch_bounds__(kThreadsTC, 1)

@@ -54,7 +54,6 @@ __global__ void __launch_bounds__(kAllocThreads)
                     int* status) {
   __shared__ int s_off[kMaxReq + 1];
   __shared__ int s_scan[32];
-  __shared__ int s_total;
   const int tid = threadIdx.x;
 
   // exclusive offsets of the requests (n_req <= kMaxReq)

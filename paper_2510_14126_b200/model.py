@@ -209,6 +209,9 @@ class GpuWorker:
         self.qmap = ops.QMap(self.q, cfg.n_heads, cfg.group)
         self.overlap_cascade = True
         self.cascade_slots = int(os.environ.get("CORTEX_CASCADE_SLOTS", "2"))
+        # balanced decode plan (equal tile ranges per CTA) instead of per-call 512-token
+        # splits; measured slower on config-2 contexts (benchmarks/attn_step.py), so opt-in
+        self.flat_decode = os.environ.get("CORTEX_FLAT_DECODE", "0") == "1"
         self.side = torch.cuda.Stream(device=dev)
         self._ev_fork = torch.cuda.Event()
         self._ev_join = torch.cuda.Event()
@@ -372,28 +375,38 @@ class GpuWorker:
         if n_out > self.max_out:
             raise ValueError("too many output rows in one step")
         garr = np.asarray(groups, i32).reshape(-1, 4).T.copy() if groups else np.zeros((4, 0), i32)
+        pslots = 0
+        if n_dec and groups:
+            # prefix partial slots (each a run of key tiles of the cascade pass)
+            pslots = min(self.cascade_slots,
+                         int(((garr[1] + BLOCK_TOKENS - 1) // BLOCK_TOKENS + 15).max() // 16))
+        fplan = None
+        if n_dec and self.flat_decode:
+            fplan = ops.decode_flat_plan(dec_prefix, dec_kvlen, cfg.n_kv_heads, bool(groups),
+                                        self.max_splits - pslots)
+        tstart = fplan[0] if fplan is not None else np.zeros(0, i32)
         (d_pos, d_arow, d_acol, d_aoff, d_tok, d_drow, d_dpre, d_dkv, d_prow, d_ppre, d_pkv,
-         d_pqs, d_pql, d_orow, d_oslot, d_ohist, d_grow, d_gplen, d_gfirst, d_gcount) = self._upload([
+         d_pqs, d_pql, d_orow, d_oslot, d_ohist, d_grow, d_gplen, d_gfirst, d_gcount,
+         d_tstart) = self._upload([
             pos, app_row, app_col, app_off, tok_ids, dec_row, dec_prefix, dec_kvlen, pf_row,
             pf_prefix, pf_kvlen, pf_qstart, pf_qlen, np.asarray(out_rows, i32),
             np.asarray(out_slot, i32), np.asarray(out_hist, i32), garr[0], garr[1], garr[2],
-            garr[3]])
+            garr[3], tstart])
         max_splits = 1
         dec_groups = None
+        flat = (d_tstart, fplan[1], fplan[2]) if fplan is not None else None
         if n_dec:
-            if groups:
-                npb = (dec_prefix + BLOCK_TOKENS - 1) // BLOCK_TOKENS
-                ntl = npb + (dec_kvlen - dec_prefix + BLOCK_TOKENS - 1) // BLOCK_TOKENS
-                priv = int(((ntl - npb + 15) // 16).max())
-                # prefix partial slots: up to 4 (each a run of key tiles of the cascade pass)
-                pslots = min(self.cascade_slots,
-                             int(((garr[1] + BLOCK_TOKENS - 1) // BLOCK_TOKENS + 15).max() // 16))
-                max_splits = pslots + priv
-                dec_groups = (d_grow, d_gplen, d_gfirst, d_gcount, len(groups), int(garr[3].max()),
-                              pslots)
+            if fplan is not None:
+                max_splits = pslots + fplan[3]
+            elif groups:  # private tokens only: splits of a prefix-less sequence
+                max_splits = pslots + max(ops.decode_splits(0, int(b - a))
+                                          for a, b in zip(dec_prefix, dec_kvlen))
             else:
                 max_splits = max(ops.decode_splits(int(a), int(b))
                                  for a, b in zip(dec_prefix, dec_kvlen))
+            if groups:
+                dec_groups = (d_grow, d_gplen, d_gfirst, d_gcount, len(groups), int(garr[3].max()),
+                              pslots)
             if max_splits > self.max_splits:
                 raise ValueError("decode context exceeds max_seq_tokens")
         w, wm = self.w, self.wmap
@@ -452,12 +465,14 @@ class GpuWorker:
                     self.side.wait_event(self._ev_fork)
                     ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=1,
                                           stream=self.side)
-                    ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=2)
+                    ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=2,
+                                          flat=flat)
                     self._ev_join.record(self.side)
                     main.wait_event(self._ev_join)
-                    ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=4)
+                    ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=4,
+                                          flat=flat)
                 else:
-                    ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap)
+                    ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, flat=flat)
                 if e0 is not None:
                     prof.close("attn_decode", e0, dec_bytes, dec_flops)
                 nl += 2

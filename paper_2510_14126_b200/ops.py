@@ -9,6 +9,8 @@ from __future__ import annotations
 
 import ctypes
 
+import numpy as np
+
 import torch
 
 from . import _lib
@@ -205,23 +207,53 @@ class QMap:
 def paged_decode_attn(kvmap: TensorMap, q, table, seq_row, seq_prefix, seq_kvlen, n_seqs,
                       n_kv_heads, group, k_row0, v_row0, scale, o_part, lse_part, max_splits, out,
                       groups=None, qmap: QMap | None = None, parts: int = 7,
-                      stream=None) -> None:
+                      stream=None, flat=None) -> None:
     """groups: None, or (grp_row, grp_plen, grp_first, grp_count, n_groups, max_count,
     prefix_slots) for shared-prefix (cascade) attention; qmap selects the tcgen05 cascade;
-    parts: 1 cascade pass | 2 context splits | 4 combine."""
+    parts: 1 cascade pass | 2 context splits | 4 combine; flat: None (fixed per-call
+    splits) or (seq_tile_start, total_tiles, tiles_per_chunk) from decode_flat_plan."""
     if groups is None:
         g = (None, None, None, None, 0, 0, 0)
     else:
         g = (_ptr(groups[0]), _ptr(groups[1]), _ptr(groups[2]), _ptr(groups[3])) + tuple(groups[4:])
+    f = (None, 0, 0) if flat is None else (_ptr(flat[0]), int(flat[1]), int(flat[2]))
     _check(
-        lib().cortex_paged_decode_attn_parts(
+        lib().cortex_paged_decode_attn_flat(
             kvmap.ptr, q.data_ptr(), table.data_ptr(), table.stride(0), seq_row.data_ptr(),
-            seq_prefix.data_ptr(), seq_kvlen.data_ptr(), n_seqs, n_kv_heads, group, k_row0,
+            seq_prefix.data_ptr(), seq_kvlen.data_ptr(), *f, n_seqs, n_kv_heads, group, k_row0,
             v_row0, scale, o_part.data_ptr(), lse_part.data_ptr(), max_splits, out.data_ptr(),
             *g, qmap.ptr if qmap is not None else None, parts, _stream(stream),
         ),
         "cortex_paged_decode_attn",
     )
+
+
+FLAT_MAX_W = 48  # kFlatMaxW in attention.cu
+
+
+def decode_flat_plan(seq_prefix, seq_kvlen, n_kv_heads: int, cascade: bool, max_pieces: int,
+                     W: int | None = None):
+    """Host half of the balanced decode plan (numpy int arrays in): (per-call flat tile
+    starts, total tiles, tiles per chunk, most slots a call's pieces need), or None when
+    the calls would need more than `max_pieces` slots each even at the widest chunk."""
+    prefix = np.asarray(seq_prefix, np.int64)
+    kvlen = np.asarray(seq_kvlen, np.int64)
+    if len(prefix) == 0:
+        return None
+    npb = (prefix + 15) // 16
+    n = (kvlen - prefix + 15) // 16 + (0 if cascade else npb)
+    start = np.zeros_like(n)
+    np.cumsum(n[:-1], out=start[1:])
+    total = int(n.sum())
+    if W is None:
+        W = int(lib().cortex_decode_tiles_per_chunk(total, n_kv_heads))
+    pieces = int(((start + n - 1) // W - start // W + 1).max())
+    if pieces > max_pieces:  # widen the chunks: a call spans <= ceil(n / W) + 1 of them
+        W = min(FLAT_MAX_W, max(W, -(-int(n.max()) // max(max_pieces - 1, 1))))
+        pieces = int(((start + n - 1) // W - start // W + 1).max())
+        if pieces > max_pieces:
+            return None
+    return start.astype(np.int32), total, W, pieces
 
 
 def fmha_prefill(kvmap: TensorMap, qmap: QMap, out, table, seq_row, seq_prefix, seq_kvlen,

@@ -190,7 +190,8 @@ def _seq_specs(rng, nb, max_blocks):
 
 
 @pytest.mark.parametrize("group", [4, 2])
-def test_paged_decode_attention(cuda, group):
+@pytest.mark.parametrize("flat", [False, True])
+def test_paged_decode_attention(cuda, group, flat):
     o = ops()
     hkv, L, nb, max_blocks = 2, 2, 512, 128
     hq = hkv * group
@@ -206,6 +207,12 @@ def test_paged_decode_attention(cuda, group):
     seq_prefix = torch.tensor([s[0] for s in specs], dtype=torch.int32, device=cuda)
     seq_kvlen = torch.tensor([s[1] for s in specs], dtype=torch.int32, device=cuda)
     max_splits = max(o.decode_splits(p, k) for p, k in specs)
+    plan = None
+    if flat:  # balanced plan: equal flat tile ranges per CTA, calls split across chunks
+        st, total, W, pieces = o.decode_flat_plan([s[0] for s in specs], [s[1] for s in specs],
+                                                  hkv, False, 64)
+        plan = (torch.as_tensor(st, device=cuda), total, W)
+        max_splits = pieces
     q = torch.randn(B, hq, 128, device=cuda).to(torch.bfloat16)
     o_part = torch.empty(B, max_splits, hq, 128, device=cuda)
     lse_part = torch.empty(B, max_splits, hq, device=cuda)
@@ -214,7 +221,7 @@ def test_paged_decode_attention(cuda, group):
     for layer in range(L):
         k0, v0 = _rows(layer, nb, hkv)
         o.paged_decode_attn(kvmap, q, table, seq_row, seq_prefix, seq_kvlen, B, hkv, group, k0, v0,
-                            1 / math.sqrt(128), o_part, lse_part, max_splits, out)
+                            1 / math.sqrt(128), o_part, lse_part, max_splits, out, flat=plan)
         torch.cuda.synchronize()
         for b, (prefix, kvlen) in enumerate(specs):
             k, v = _logical_kv(cache, layer, table[b].cpu(), prefix, kvlen)
@@ -225,7 +232,7 @@ def test_paged_decode_attention(cuda, group):
 
 @pytest.mark.parametrize("group", [4, 2])
 @pytest.mark.parametrize("plens", [(1000, 40), (8192,), (16, 5, 0)])
-@pytest.mark.parametrize("impl", ["mma", "tc"])
+@pytest.mark.parametrize("impl", ["mma", "tc", "tc-flat"])
 def test_cascade_decode_attention(cuda, group, plens, impl):
     """Shared-prefix decode: calls grouped by resident prefix, prefix attended once."""
     o = ops()
@@ -266,6 +273,11 @@ def test_cascade_decode_attention(cuda, group, plens, impl):
     pslots = max([((P + 15) // 16 + 15) // 16 for _, P, _, _ in grp] + [1])
     priv = max(((kv - p) + 255) // 256 for p, kv in zip(seq_pre, seq_kv))
     max_splits = pslots + priv
+    plan = None
+    if impl == "tc-flat":
+        st, total, W, pieces = o.decode_flat_plan(seq_pre, seq_kv, hkv, True, 64)
+        plan = (torch.as_tensor(st, device=cuda), total, W)
+        max_splits = pslots + pieces
     q = torch.randn(B, hq, 128, device=cuda).to(torch.bfloat16)
     o_part = torch.empty(B, max_splits, hq, 128, device=cuda)
     lse_part = torch.empty(B, max_splits, hq, device=cuda)
@@ -276,7 +288,7 @@ def test_cascade_decode_attention(cuda, group, plens, impl):
     o.paged_decode_attn(o.kv_map(cache.view(-1, 128)), q, table, dev(seq_row), dev(seq_pre),
                         dev(seq_kv), B, hkv, group, k0, v0, 1 / math.sqrt(128), o_part, lse_part,
                         max_splits, out, groups=groups,
-                        qmap=o.QMap(q, hq, group) if impl == "tc" else None)
+                        qmap=o.QMap(q, hq, group) if impl != "mma" else None, flat=plan)
     torch.cuda.synchronize()
     for b in range(B):
         k, v = _logical_kv(cache, 0, table[seq_row[b]].cpu(), seq_pre[b], seq_kv[b])

@@ -32,7 +32,9 @@ def test_library_loads_and_exports_everything():
     assert lib.cortex_abi_version() == 100
     # pure host helpers are callable without a GPU
     assert lib.cortex_gemm_splits(32, 6144, 4096) >= 1
-    assert lib.cortex_decode_splits(1000, 1300) == 6
+    assert lib.cortex_decode_splits(1000, 1300) == 3  # 82 tiles in 32-tile splits
+    # balanced plan: 2 waves of 55 chunks x 8 kv heads on 148 SMs -> 37 tiles per chunk
+    assert lib.cortex_decode_tiles_per_chunk(4000, 8) == 37
     assert lib.cortex_gemm_path(700, 4096, 4096) == 2
     assert lib.cortex_gemm_path(64, 4096, 4096) == 1
 
