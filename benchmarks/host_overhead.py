@@ -1,0 +1,72 @@
+"""Is a config-2 step GPU-bound or host-bound?
+
+Runs the bench runtime and splits the host wall time of each step into: time the
+host spent blocked on the GPU (waiting for a staging-ring slot, i.e. the GPU is
+behind), time inside GpuWorker.forward (Python + launches), and scheduler time
+(dispatch, planning, completions). If "blocked" is a large share, the GPU is the
+bottleneck; if it is near zero the host is.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def main(steps: int = 300) -> None:
+    torch.cuda.set_device(0)
+    rt, cfg, _ = bench.build_runtime("llama3-8b", "config2", 256, torch.device("cuda", 0), 0, 1)
+    w = rt.worker
+    rt.fill()
+    rt.run_steps(150)
+    torch.cuda.synchronize()
+    acc = {"blocked": 0.0, "forward": 0.0}
+    evts = w.meta_evt
+
+    class TimedEvent:
+        def __init__(self, e):
+            self.e = e
+
+        def synchronize(self):
+            t = time.perf_counter()
+            self.e.synchronize()
+            acc["blocked"] += time.perf_counter() - t
+
+        def query(self):
+            return self.e.query()
+
+    orig_fwd = w.forward
+
+    def fwd(plan):
+        t = time.perf_counter()
+        r = orig_fwd(plan)
+        acc["forward"] += time.perf_counter() - t
+        return r
+
+    w.forward = fwd
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        for i, e in enumerate(evts):
+            if e is not None and not isinstance(e, TimedEvent):
+                evts[i] = TimedEvent(e)
+        rt.step()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    out = {"steps": steps, "wall_ms_per_step": 1e3 * wall / steps,
+           "blocked_ms_per_step": 1e3 * acc["blocked"] / steps,
+           "forward_ms_per_step (incl. blocked)": 1e3 * acc["forward"] / steps,
+           "scheduler_ms_per_step": 1e3 * (wall - acc["forward"]) / steps}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -15,10 +15,13 @@
 //   warp 1      MMA issuer (one thread): S_t = Q K_t^T  (M=128, N=128, K=128) into
 //               one of two TMEM S buffers; O += P_{t-1} V_{t-1}  (A = P from smem,
 //               K-major; B = V from smem, MN-major) into the TMEM O accumulator
-//   warps 2..5  softmax: thread = query row = TMEM lane; S row -> mask -> running
-//               max (rescale O in TMEM only when the max grows by > 2^8) -> P (bf16)
-//               into smem -> final O / l (bf16 output, or fp32 partial + LSE)
+//   warps 2..9  softmax, two warps per TMEM lane quarter: thread = (query row, half
+//               of the tile's keys); S -> mask -> running max agreed between the two
+//               halves (rescale O in TMEM only when the max grows by > 2^8) -> P as
+//               bf16 hi + lo back into TMEM -> final O / l (bf16 output, or fp32
+//               partial + LSE), each half emitting 64 of the 128 dims
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -28,7 +31,7 @@ constexpr int kHD = 128;
 constexpr int kBlk = 16;
 constexpr int kBlocksPerTile = 8;  // 128 keys
 constexpr int kRows = 128;
-constexpr int kThreadsTC = 192;
+constexpr int kThreadsTC = 320;  // TMA, MMA, 8 softmax warps
 constexpr float kLog2eTC = 1.4426950408889634f;
 constexpr float kRescaleThresh = 8.0f;  // log2 units
 
@@ -39,7 +42,8 @@ constexpr int kStagesTC = 2;
 constexpr int kOffQ = 0;
 constexpr int kOffKV = kQBytes;
 constexpr int kOffBar = kOffKV + kStagesTC * kKVStage;
-constexpr int kSmemTC = kOffBar + 256 + 1024;
+constexpr int kOffX = kOffBar + 256;  // row-max / row-sum exchange of the softmax halves
+constexpr int kSmemTC = kOffX + 6 * 128 * 4 + 1024;
 constexpr uint32_t kTmemColsTC = 512;  // S0 [0,128) S1 [128,256) O [256,384)
 
 struct FmhaArgs {
@@ -66,6 +70,7 @@ struct FmhaArgs {
   float* o_part;
   float* lse_part;
   int max_splits;
+  int p_lo;  // 1: P enters PV as bf16 hi + lo (~2^-17), 0: bf16 P only
 };
 
 struct BlockRef {
@@ -200,6 +205,16 @@ CORTEX_DEVICE void mbar_wait_guard(uint64_t* bar, uint32_t parity) {
   }
 }
 
+CORTEX_DEVICE void named_bar_sync(int id, int n_threads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n_threads) : "memory");
+}
+
+CORTEX_DEVICE float ex2_approx(float x) {  // 2^x, one MUFU op (-inf -> 0)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __global__ void __launch_bounds__(kThreadsTC, 1)
     fmha_tc_kernel(const __grid_constant__ CUtensorMap tmap_q,
                    const __grid_constant__ CUtensorMap tmap_kv, const FmhaArgs a) {
@@ -273,7 +288,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       mbar_init(&v_empty[s], 1);
       mbar_init(&s_full[s], 1);
     }
-    mbar_init(p_full, 4);
+    mbar_init(p_full, 8);
     mbar_init(o_ready, 1);
     mbar_init(o_done, 1);
     fence_mbar_init();
@@ -355,7 +370,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           // S buffer it was computed from (A operand from TMEM, 8 columns per 16 keys)
           const uint32_t p_tmem = tmem_s + 128 * s;
 #pragma unroll
-          for (int part = 0; part < 2; ++part) {
+          for (int part = 0; part < 1 + a.p_lo; ++part) {
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
               umma_bf16_ts(tmem_o, p_tmem + 64 * part + 8 * kk,
@@ -370,22 +385,30 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
     }
   } else {
-    // ---- softmax warps: thread <-> query row (TMEM lane) ----
+    // ---- softmax warps 2..9: thread <-> (query row, half of the key columns) ----
+    // Warps w and w+4 share TMEM lane quarter w % 4 (the same 32 rows) and split every
+    // S row: half 0 owns keys [0, 64) of the tile, half 1 keys [64, 128). They agree on
+    // the row max through shared memory (one named barrier per quarter), keep partial
+    // row sums, and each rescales / emits its own 64 of the 128 O dims.
     const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int r = quad * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const bool row_ok = r < ntok * group;
     const int qpos = qpos_base + r / group;
+    float* xmax = reinterpret_cast<float*>(smem + kOffX);  // [2 slots][2 halves][128 rows]
+    float* xsum = xmax + 4 * kRows;                         // [2 halves][128 rows]
+    const int bar_id = 1 + quad;
     float m_run = -INFINITY, l_run = 0.f;
     for (int kt = 0; kt < n_kt; ++kt) {
       const int s = kt % kStagesTC;
       mbar_wait_guard(&s_full[s], (kt / kStagesTC) & 1);
       tc_fence_after();
-      float sv[128];
+      float sv[64];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t u[32];
-        tmem_ld_x32(tmem_s + 128 * s + lane_off + 32 * c, u);
+        tmem_ld_x32(tmem_s + 128 * s + lane_off + 64 * half + 32 * c, u);
         tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 32; ++i) sv[32 * c + i] = __uint_as_float(u[i]);
@@ -403,11 +426,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       float mraw = -INFINITY;
       if (full) {
 #pragma unroll
-        for (int i = 0; i < 128; ++i) mraw = fmaxf(mraw, sv[i]);
+        for (int i = 0; i < 64; ++i) mraw = fmaxf(mraw, sv[i]);
       } else {
 #pragma unroll
-        for (int j = 0; j < kBlocksPerTile; ++j) {
-          const BlockSpan b = block_span(prefix_len, kv_len, j0 + j, blk_end);
+        for (int j = 0; j < kBlocksPerTile / 2; ++j) {
+          const BlockSpan b = block_span(prefix_len, kv_len, j0 + 4 * half + j, blk_end);
 #pragma unroll
           for (int i = 0; i < kBlk; ++i) {
             const bool ok = row_ok && i < b.nvalid && b.pos0 + i <= qpos;
@@ -416,6 +439,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           }
         }
       }
+      xmax[((kt & 1) * 2 + half) * kRows + r] = mraw;
+      named_bar_sync(bar_id, 64);
+      mraw = fmaxf(mraw, xmax[((kt & 1) * 2 + (half ^ 1)) * kRows + r]);
       const float mt = mraw * a.scale_log2;  // -inf stays -inf
       // running max: adopt the tile max when the row had none yet (its O row is 0), or
       // when it grew by more than 2^8 (then O and l are rescaled); otherwise keep the
@@ -427,54 +453,64 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       // p = exp2(s * scale - m), computed before waiting for the previous PV
       float lsum = 0.f;
 #pragma unroll
-      for (int i = 0; i < 128; ++i) {
-        sv[i] = exp2f(fmaf(sv[i], a.scale_log2, -m_use));
+      for (int i = 0; i < 64; ++i) {
+        sv[i] = ex2_approx(fmaf(sv[i], a.scale_log2, -m_use));
         lsum += sv[i];
       }
-      // O rescale (rare; tcgen05.ld/st are warp-collective: decided per warp, alpha per
-      // row) needs PV of the previous tile finished
+      // O rescale of this half's 64 dims (rare; tcgen05.ld/st are warp-collective:
+      // decided per warp - the partner warp sees the same rows - alpha per row) needs
+      // PV of the previous tile finished
       if (kt > 0 && __any_sync(0xffffffffu, adopt && m_run != -INFINITY)) {
         mbar_wait_guard(o_ready, (kt - 1) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 2; ++c) {
           uint32_t u[32];
-          tmem_ld_x32(tmem_o + lane_off + 32 * c, u);
+          tmem_ld_x32(tmem_o + lane_off + 64 * half + 32 * c, u);
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * alpha);
-          tmem_st_x32(tmem_o + lane_off + 32 * c, u);
+          tmem_st_x32(tmem_o + lane_off + 64 * half + 32 * c, u);
         }
         tmem_st_wait();
       }
       l_run = l_run * alpha + lsum;
       m_run = m_new;
-      // P (bf16 hi + lo, keys 2c / 2c+1 packed in column c) -> TMEM over this S buffer
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      // P (bf16 hi + lo, keys 2c / 2c+1 packed in column c) -> TMEM over this S buffer:
+      // hi of keys [64 half, +64) in columns [32 half, +32), lo 64 columns further
+      {
         uint32_t hi[32], lo[32];
+        if (a.p_lo) {
 #pragma unroll
-        for (int c = 0; c < 32; ++c) split_bf16(sv[64 * h + 2 * c], sv[64 * h + 2 * c + 1], hi[c], lo[c]);
-        tmem_st_x32(tmem_s + 128 * s + lane_off + 32 * h, hi);
-        tmem_st_x32(tmem_s + 128 * s + lane_off + 64 + 32 * h, lo);
+          for (int c = 0; c < 32; ++c) split_bf16(sv[2 * c], sv[2 * c + 1], hi[c], lo[c]);
+          tmem_st_x32(tmem_s + 128 * s + lane_off + 32 * half, hi);
+          tmem_st_x32(tmem_s + 128 * s + lane_off + 64 + 32 * half, lo);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) hi[c] = pack_bf16(sv[2 * c], sv[2 * c + 1]);
+          tmem_st_x32(tmem_s + 128 * s + lane_off + 32 * half, hi);
+        }
       }
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
     }
-    // ---- epilogue ----
+    // ---- epilogue: row sum of both halves, then this half's 64 O dims ----
+    xsum[half * kRows + r] = l_run;
+    named_bar_sync(bar_id, 64);
+    const float l_tot = l_run + xsum[(half ^ 1) * kRows + r];
     mbar_wait_guard(o_done, 0);
     tc_fence_after();
     const int tok = tok0 + r / group;
     const int h = kvh * group + r % group;
-    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+    const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
     if (a.mode == 0) {
-      __nv_bfloat16* orow = a.out + (static_cast<int64_t>(tok) * hq + h) * kHD;
+      __nv_bfloat16* orow = a.out + (static_cast<int64_t>(tok) * hq + h) * kHD + 64 * half;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t u[32];
-        tmem_ld_x32(tmem_o + lane_off + 32 * c, u);
+        tmem_ld_x32(tmem_o + lane_off + 64 * half + 32 * c, u);
         tmem_ld_wait();
         if (row_ok) {
 #pragma unroll
@@ -491,11 +527,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     } else {
       const int ps = item % a.max_psplits;
       const int64_t pidx = (static_cast<int64_t>(tok) * a.max_splits + ps) * hq + h;
-      float* o = a.o_part + pidx * kHD;
+      float* o = a.o_part + pidx * kHD + 64 * half;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t u[32];
-        tmem_ld_x32(tmem_o + lane_off + 32 * c, u);
+        tmem_ld_x32(tmem_o + lane_off + 64 * half + 32 * c, u);
         tmem_ld_wait();
         if (row_ok) {
 #pragma unroll
@@ -505,10 +541,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                             __uint_as_float(u[i + 2]) * inv, __uint_as_float(u[i + 3]) * inv);
         }
       }
-      if (row_ok) a.lse_part[pidx] = m_run + log2f(l_run);
+      if (row_ok && half == 0) a.lse_part[pidx] = m_run + log2f(l_tot);
     }
   }
-
   __syncwarp();
   tc_fence_before();
   __syncthreads();
@@ -516,6 +551,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     tc_fence_after();
     tmem_dealloc(tmem, kTmemColsTC);
   }
+}
+
+// CORTEX_FMHA_PLO=0 drops the lo half of P (one PV pass instead of two).
+int fmha_p_lo() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CORTEX_FMHA_PLO");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v;
 }
 
 int32_t launch_fmha(const CUtensorMap* tq, const CUtensorMap* tkv, const FmhaArgs& a, dim3 grid,
@@ -555,6 +600,7 @@ int32_t cortex_fmha_prefill_tc(const void* tmap_kv, const void* tmap_q, void* ou
   a.v_row0 = v_row0;
   a.scale_log2 = softmax_scale * kLog2eTC;
   a.mode = 0;
+  a.p_lo = fmha_p_lo();
   a.seq_row = seq_row;
   a.seq_prefix = seq_prefix;
   a.seq_kvlen = seq_kvlen;
@@ -588,6 +634,7 @@ int32_t cortex_fmha_cascade_tc(const void* tmap_kv, const void* tmap_q, const in
   a.v_row0 = v_row0;
   a.scale_log2 = softmax_scale * kLog2eTC;
   a.mode = 1;
+  a.p_lo = fmha_p_lo();
   a.grp_row = grp_row;
   a.grp_plen = grp_plen;
   a.grp_first = grp_first;

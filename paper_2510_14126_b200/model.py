@@ -85,9 +85,13 @@ class KernelProfile:
 
     Each record: (class, start event, end event, algorithmic bytes, flops)."""
 
-    def __init__(self, classes) -> None:
+    def __init__(self, classes, every: int = 1) -> None:
         self.classes = set(classes)
         self.recs: list = []
+        self.every = every  # time the kernels of one step in `every` (event overhead)
+
+    def sampled(self, step: int) -> bool:
+        return step % self.every == 0
 
     def open(self, cls):
         if cls not in self.classes:
@@ -421,7 +425,7 @@ class GpuWorker:
             nl += 1
         o_part = self.o_part[: max(n_dec, 1) * max_splits * hq * HEAD_DIM]
         lse_part = self.lse_part[: max(n_dec, 1) * max_splits * hq]
-        prof = self.prof
+        prof = self.prof if self.prof is not None and self.prof.sampled(self.steps) else None
         tok_kv_bytes = hkv * HEAD_DIM * 2 * 2  # K + V of one token in one layer
         if prof is not None:
             uniq = sum(d.kv_len - d.prefix_len for d in plan.decode)
