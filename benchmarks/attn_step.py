@@ -79,7 +79,7 @@ def build(n_calls=215, n_pf=3, pf_len=200, slots=2, seed=0, layers=4):
     plan = ops.decode_flat_plan(np.full(n_calls, P), P + priv, HKV, True, 64)
     st["flat_plan"] = (d(plan[0]), plan[1], plan[2])
     st["flat_W"] = plan[2]
-    st["flat"] = st["flat_plan"] if os.environ.get("CORTEX_FLAT_DECODE", "1") != "0" else None
+    st["flat"] = st["flat_plan"] if os.environ.get("CORTEX_FLAT_DECODE", "0") == "1" else None
     persplit = max(ops.decode_splits(0, int(p)) for p in priv)
     st["max_splits"] = st["max_splits_cap"] = slots + max(persplit, plan[3], 8)
     st["o_part"] = torch.empty(n_calls * st["max_splits"] * HQ * 128, device=dev)
@@ -118,6 +118,20 @@ def decode_overlap(st, layer):
     st["ev"][0].record(main)
     st["side"].wait_event(st["ev"][0])
     decode(st, layer, 1, st["side"])
+    decode(st, layer, 2)
+    st["ev"][1].record(st["side"])
+    main.wait_event(st["ev"][1])
+    decode(st, layer, 4)
+
+
+def layer_side_prefill(st, layer):
+    """Cascade pass then prefill FMHA (both tensor-bound) on the side stream, concurrent
+    with the private-context decode splits (HBM-bound) on the main stream."""
+    main = torch.cuda.current_stream()
+    st["ev"][0].record(main)
+    st["side"].wait_event(st["ev"][0])
+    decode(st, layer, 1, st["side"])
+    prefill(st, layer, st["side"])
     decode(st, layer, 2)
     st["ev"][1].record(st["side"])
     main.wait_event(st["ev"][1])
@@ -178,6 +192,7 @@ def main():
         "decode_overlap_us": timed(st, lambda l: decode_overlap(st, l)),
         "prefill_us": timed(st, lambda l: prefill(st, l)),
         "layer_us": timed(st, lambda l: (decode_overlap(st, l), prefill(st, l))),
+        "layer_side_prefill_us": timed(st, lambda l: layer_side_prefill(st, l)),
     }
     priv_bytes = st["priv_tokens"] * HKV * 128 * 2 * 2
     res["private_GBps"] = priv_bytes / res["private_us"] / 1e3

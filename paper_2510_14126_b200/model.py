@@ -456,19 +456,36 @@ class GpuWorker:
             ops.rope_kv_append(self.qkv, self.q, self.cache, k0, v0, self.table, d_pos, d_arow,
                                d_acol, d_aoff, self.cos, self.sin, T, hq, hkv)
             nl += 3
+            def prefill_attn(stream=None):
+                if self.tc_attention:
+                    ops.fmha_prefill(self.kvmap, self.qmap, self.attn, self.table, d_prow, d_ppre,
+                                     d_pkv, d_pqs, d_pql, n_pf, max_qlen, hkv, cfg.group, k0, v0,
+                                     self.scale, stream=stream)
+                else:
+                    ops.paged_prefill_attn(self.kvmap, self.q, self.attn, self.table, d_prow,
+                                           d_ppre, d_pkv, d_pqs, d_pql, n_pf, max_qlen, hkv,
+                                           cfg.group, k0, v0, self.scale, stream=stream)
+
+            pf_done = False
             if n_dec:
                 e0 = prof.open("attn_decode") if prof is not None else None
                 dargs = (self.kvmap, self.q, self.table, d_drow, d_dpre, d_dkv, n_dec, hkv,
                          cfg.group, k0, v0, self.scale, o_part, lse_part, max_splits, self.attn)
                 qmap = self.qmap if self.tc_attention else None
                 if dec_groups is not None and qmap is not None and self.overlap_cascade:
-                    # shared-prefix pass (tensor cores, L2) on a side stream, concurrent with
-                    # the per-call context splits (HBM); join before the LSE combine
+                    # tensor-core passes - the shared-prefix (cascade) pass, then the prompt
+                    # prefill - on a side stream, concurrent with the per-call context splits
+                    # (HBM) on the main stream; join before the LSE combine. (The decode
+                    # profile window then covers the prefill attention too.)
                     main = torch.cuda.current_stream()
                     self._ev_fork.record(main)
                     self.side.wait_event(self._ev_fork)
                     ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=1,
                                           stream=self.side)
+                    if n_pf:
+                        prefill_attn(self.side)
+                        pf_done = True
+                        nl += 1
                     ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=2,
                                           flat=flat)
                     self._ev_join.record(self.side)
@@ -478,18 +495,12 @@ class GpuWorker:
                 else:
                     ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, flat=flat)
                 if e0 is not None:
-                    prof.close("attn_decode", e0, dec_bytes, dec_flops)
+                    prof.close("attn_decode", e0, dec_bytes + (pf_bytes if pf_done else 0.0),
+                               dec_flops + (pf_flops if pf_done else 0.0))
                 nl += 2
-            if n_pf:
+            if n_pf and not pf_done:
                 e0 = prof.open("attn_prefill") if prof is not None else None
-                if self.tc_attention:
-                    ops.fmha_prefill(self.kvmap, self.qmap, self.attn, self.table, d_prow, d_ppre,
-                                     d_pkv, d_pqs, d_pql, n_pf, max_qlen, hkv, cfg.group, k0, v0,
-                                     self.scale)
-                else:
-                    ops.paged_prefill_attn(self.kvmap, self.q, self.attn, self.table, d_prow,
-                                           d_ppre, d_pkv, d_pqs, d_pql, n_pf, max_qlen, hkv,
-                                           cfg.group, k0, v0, self.scale)
+                prefill_attn()
                 if e0 is not None:
                     prof.close("attn_prefill", e0, pf_bytes, pf_flops)
                 nl += 1
