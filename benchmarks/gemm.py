@@ -51,7 +51,8 @@ def bench(M: int, name: str, iters: int = 20, residual: bool = False) -> dict:
     flops = 2.0 * M * N * K
     return {"M": M, "name": name, "residual": residual, "ms": ms, "tflops": flops / ms / 1e9,
             "weight_GBps": N * K * 2 / ms / 1e6, "cublas_ms": ms_cublas,
-            "cublas_tflops": flops / ms_cublas / 1e9, "splits": ops.gemm_splits(M, N, K)}
+            "cublas_tflops": flops / ms_cublas / 1e9, "splits": ops.gemm_splits(M, N, K),
+            "path": ops.gemm_path(M, N, K), "tile2": ops.lib().cortex_gemm2_tile(M, N, K)}
 
 
 if __name__ == "__main__":

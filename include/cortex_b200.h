@@ -102,6 +102,12 @@ int32_t cortex_gemm_splits(int32_t M, int32_t N, int32_t K);
 int32_t cortex_gemm_path(int32_t M, int32_t N, int32_t K);
 /* Test hook: 0 = automatic, 1 = force the 1-SM kernel, 2 = force 2-SM when legal. */
 int32_t cortex_gemm_set_mode(int32_t mode);
+/* 2-SM kernel scheduling: -1 = automatic, 0 = whole tiles, 1 = stream-K (equal K-block
+ * ranges per CTA pair; partial tiles reduced through workspace, deterministic). The
+ * workspace must hold SMs x 256 x 128 floats and the counters SMs ints (zeroed). */
+int32_t cortex_gemm_set_stream_k(int32_t force);
+/* The 2-SM kernel's plan for (M, N, K): TN | (stream_k << 16). */
+int32_t cortex_gemm2_tile(int32_t M, int32_t N, int32_t K);
 int32_t cortex_gemm_bf16(const void* tmap_w, const void* tmap_x, int32_t M, int32_t N, int32_t K,
                          void* out, int32_t ldo, int32_t out_f32, const void* residual,
                          int32_t ldr, float* workspace, uint64_t workspace_bytes,

@@ -13,6 +13,19 @@
 // optional fp32 residual) while the MMA warp already accumulates tile i + 1.
 // Pairs are persistent and walk tiles m-fastest, so concurrently running pairs
 // share weight tiles in L2.
+//
+// Stream-K mode (when tiles do not fill whole waves of pairs, e.g. the N = 4096
+// projections at M ~ 700: 64 tiles for 74 pairs): the tiles' K blocks are laid
+// end to end and pair p takes the contiguous range [p U / P, (p+1) U / P) of the
+// U = tiles x K-blocks units, so every pair does the same MMA work. A pair whose
+// range starts inside a tile writes that partial accumulator to a per-pair
+// workspace slot and raises a flag; the pair holding the tile's first K blocks
+// (it reaches them last) waits for the flags and adds the partials in pair order
+// (deterministic) before its epilogue. Pairs only ever wait on later pairs'
+// first segments, which those pairs compute first, so the grid (all pairs
+// resident) cannot deadlock.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace {
@@ -22,11 +35,6 @@ constexpr int kBK = 64;
 constexpr int kXBox2 = 16;   // activation rows per TMA box
 constexpr int kEpiRows = 32; // output rows (m) per epilogue chunk
 constexpr int kThreads2 = 192;
-// K splits for the compute-bound GEMM: the deterministic fix-up (partials through L2 + a
-// last-unit reduction) cost more than the wave-quantization it removes at the measured
-// shapes (M=700, N=4096: 70 us split vs 37 us unsplit), so it is off.
-constexpr int kMaxSplits2 = 1;
-
 struct Gemm2Args {
   int M, N, K;
   void* out;
@@ -36,11 +44,42 @@ struct Gemm2Args {
   int ldr;
   int m_tiles;
   int num_tiles;
-  int splits;        // K splits per tile (work units = num_tiles * splits)
-  int kb_per_split;
-  float* workspace;  // [splits][M][N] fp32 partials (splits > 1)
-  int* counters;     // [num_tiles * 2] arrival counters, left zeroed
+  int npairs;        // persistent CTA pairs (grid / 2)
+  int sk;            // 1: stream-K ranges, 0: whole tiles round-robin
+  int total_units;   // num_tiles * K blocks
+  float* workspace;  // stream-K: [npairs * 2][TN][128] fp32 partials
+  int* flags;        // stream-K: [npairs * 2] partial-ready flags, left zeroed
 };
+
+struct Seg {
+  int t, kb0, kb1;  // tile, K-block range
+};
+
+CORTEX_DEVICE int sk_begin(const Gemm2Args& a, int p) {
+  return static_cast<int>(static_cast<long long>(p) * a.total_units / a.npairs);
+}
+
+// Next segment of a pair's work; `pos` starts at seg_start() and is advanced.
+CORTEX_DEVICE int seg_start(const Gemm2Args& a, int pair) { return a.sk ? sk_begin(a, pair) : pair; }
+
+CORTEX_DEVICE bool seg_next(const Gemm2Args& a, int pair, int& pos, Seg& g) {
+  const int tkb = a.K / kBK;
+  if (!a.sk) {
+    if (pos >= a.num_tiles) return false;
+    g.t = pos;
+    g.kb0 = 0;
+    g.kb1 = tkb;
+    pos += a.npairs;
+    return true;
+  }
+  const int end = sk_begin(a, pair + 1);
+  if (pos >= end) return false;
+  g.t = pos / tkb;
+  g.kb0 = pos % tkb;
+  g.kb1 = min(tkb, g.kb0 + (end - pos));
+  pos += g.kb1 - g.kb0;
+  return true;
+}
 
 template <int TN, int STAGES>
 struct G2 {
@@ -115,6 +154,36 @@ CORTEX_DEVICE void tmem_dealloc_2sm(uint32_t taddr, uint32_t ncols) {
                : "memory");
 }
 
+CORTEX_DEVICE int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+CORTEX_DEVICE void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+CORTEX_DEVICE float4 ws_load(const float4* p) { return __ldcg(p); }
+
+// Tuning builds (-DCORTEX_GEMM_TRACE): globaltimer stamps of the epilogue's segment
+// events into the tail of the workspace: [pair][rank][16] u64 at float offset 15 Mi.
+#ifdef CORTEX_GEMM_TRACE
+#define GEMM_TRACE(ev)                                                                       \
+  do {                                                                                      \
+    if (threadIdx.x == 64 && (ev) < 16) {                                                   \
+      uint64_t t_;                                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                \
+      reinterpret_cast<uint64_t*>(args.workspace + (15u << 20))[(2 * pair + rank) * 16 + (ev)] = \
+          t_;                                                                               \
+    }                                                                                       \
+  } while (0)
+#else
+#define GEMM_TRACE(ev) \
+  do {                 \
+  } while (0)
+#endif
+
 CORTEX_DEVICE void epi_bar_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
 
 // Rows ew, ew+4, ... < crow of a staged fp32 chunk -> (+ fp32 residual) -> bf16 / fp32 out.
@@ -188,10 +257,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1;
-  const int npairs = gridDim.x >> 1;
   const int warp = warp_id();
   const int lane = lane_id();
   const int total_kb = args.K / kBK;
+  GEMM_TRACE(15);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_w);
@@ -216,15 +285,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     if (elect_one()) {
       // ---- TMA producer (both CTAs load their halves) ----
       uint32_t it = 0;
-      for (int u = pair; u < args.num_tiles * args.splits; u += npairs) {
-        const int t = u / args.splits;
-        const int kb0 = (u % args.splits) * args.kb_per_split;
-        const int kb1 = min(total_kb, kb0 + args.kb_per_split);
-        const int n_tile = t / args.m_tiles;
-        const int m_tile = t % args.m_tiles;
+      int pos = seg_start(args, pair);
+      Seg g;
+      while (seg_next(args, pair, pos, g)) {
+        const int n_tile = g.t / args.m_tiles;
+        const int m_tile = g.t % args.m_tiles;
         const int n0 = n_tile * kPairN + rank * 128;
         const int x0 = m_tile * TN + rank * (TN / 2);
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        for (int kb = g.kb0; kb < g.kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
@@ -248,9 +316,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       // ---- MMA issuer (leader CTA, one thread) ----
       constexpr uint32_t idesc = umma_idesc_bf16(kPairN, TN);
       uint32_t it = 0, tl = 0;
-      for (int u = pair; u < args.num_tiles * args.splits; u += npairs, ++tl) {
-        const int kb0 = (u % args.splits) * args.kb_per_split;
-        const int kb1 = min(total_kb, kb0 + args.kb_per_split);
+      int pos = seg_start(args, pair);
+      Seg g;
+      for (; seg_next(args, pair, pos, g); ++tl) {
+        const int kb0 = g.kb0, kb1 = g.kb1;
         const uint32_t b = tl & 1;
         const uint32_t tph = (tl >> 1) & 1;
         mbar_wait(&tempty[b], tph ^ 1);
@@ -277,11 +346,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     const int quad = warp & 3;
     const int ew = warp - 2;  // 0..3
     const uint32_t tempty_leader_base = mapa_shared(smem_u32(&tempty[0]), 0);
-    int* last_flag = reinterpret_cast<int*>(tmem_holder + 1);
     uint32_t tl = 0;
-    for (int u = pair; u < args.num_tiles * args.splits; u += npairs, ++tl) {
-      const int t = u / args.splits;
-      const int z = u % args.splits;
+    int pos = seg_start(args, pair);
+    Seg g;
+    for (; seg_next(args, pair, pos, g); ++tl) {
+      const int t = g.t;
       const uint32_t b = tl & 1;
       const uint32_t tph = (tl >> 1) & 1;
       const int n_tile = t / args.m_tiles;
@@ -290,10 +359,62 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       const int m0 = m_tile * TN;
       const int rows = min(TN, args.M - m0);
       const int col = n0 + 4 * lane;
+      // stream-K roles: a segment starting inside its tile contributes a partial; the
+      // segment with the tile's first K blocks (and not its last) collects them
+      const bool contrib = g.kb0 > 0;
+      const bool head = g.kb0 == 0 && g.kb1 < total_kb;
+      int q_end = pair + 1;
+      if (head) {
+        while (q_end < args.npairs && sk_begin(args, q_end) < (t + 1) * total_kb) ++q_end;
+        if (threadIdx.x == 64) {
+          for (int q = pair + 1; q < q_end; ++q) {
+            const int* f = args.flags + 2 * q + rank;
+            while (ld_acquire_gpu(f) == 0) __nanosleep(64);
+          }
+        }
+        epi_bar_sync();
+      }
+      if (tl < 2) GEMM_TRACE(4 * static_cast<int>(tl) + 0);
       mbar_wait(&tfull[b], tph);
+      if (tl < 2) GEMM_TRACE(4 * static_cast<int>(tl) + 1);
       tc_fence_after();
       const uint32_t taddr = tmem_base + b * TN + (static_cast<uint32_t>(quad * 32) << 16);
       for (int c0 = 0; c0 < rows; c0 += kEpiRows) {
+        const int crow = min(kEpiRows, rows - c0);
+        // global operands of this chunk first (residual, stream-K partials): their round
+        // trip overlaps the TMEM read and the staging transpose
+        float4 acc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (!contrib) {
+          if (args.residual && args.out_f32 != 2) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int r = ew + 4 * q;
+              if (r < crow)
+                acc[q] = *reinterpret_cast<const float4*>(  // (out may alias: no .nc)
+                    args.residual + static_cast<size_t>(m0 + c0 + r) * args.ldr + col);
+            }
+          }
+          if (head) {  // + the later pairs' partials of this tile, in pair order
+            for (int qp = pair + 1; qp < q_end; ++qp) {
+              const float* ws = args.workspace + static_cast<size_t>(2 * qp + rank) * TN * 128;
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const int r = ew + 4 * q;
+                if (r < crow) {
+                  const float4 v = ws_load(reinterpret_cast<const float4*>(
+                      ws + static_cast<size_t>(c0 + r) * 128 + 4 * lane));
+                  acc[q].x += v.x;
+                  acc[q].y += v.y;
+                  acc[q].z += v.z;
+                  acc[q].w += v.w;
+                }
+              }
+            }
+          }
+        }
+        if (c0 == 0) GEMM_TRACE(8);
         uint32_t r0[16], r1[16];
         tmem_ld_32x32b_x16(taddr + c0, r0);
         tmem_ld_32x32b_x16(taddr + c0 + 16, r1);
@@ -304,79 +425,76 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           staging[(16 + j) * 128 + quad * 32 + lane] = __uint_as_float(r1[j]);
         }
         epi_bar_sync();
-        const int crow = min(kEpiRows, rows - c0);
-        if (args.splits == 1) {
-          store_chunk(args, staging, m0 + c0, crow, ew, lane, col);
-        } else {
-          float* ws = args.workspace + static_cast<size_t>(z) * args.M * args.N;
+        if (c0 == 0) GEMM_TRACE(9);
+        if (c0 == 32) GEMM_TRACE(10);
+        if (contrib) {
+          float* ws = args.workspace + static_cast<size_t>(2 * pair + rank) * TN * 128;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const int r = ew + 4 * q;
             if (r < crow)
-              __stcg(reinterpret_cast<float4*>(ws + static_cast<size_t>(m0 + c0 + r) * args.N + col),
+              __stcg(reinterpret_cast<float4*>(ws + static_cast<size_t>(c0 + r) * 128 + 4 * lane),
                      reinterpret_cast<const float4*>(staging + r * 128)[lane]);
+          }
+        } else if (args.out_f32 == 2) {  // SwiGLU reads other lanes' columns of the row
+          if (head) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int r = ew + 4 * q;
+              if (r < crow) {
+                float4& d = reinterpret_cast<float4*>(staging + r * 128)[lane];
+                d.x += acc[q].x;
+                d.y += acc[q].y;
+                d.z += acc[q].z;
+                d.w += acc[q].w;
+              }
+            }
+            __syncwarp();
+          }
+          store_chunk(args, staging, m0 + c0, crow, ew, lane, col);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int r = ew + 4 * q;
+            if (r < crow) {
+              const float4 v = reinterpret_cast<const float4*>(staging + r * 128)[lane];
+              const float4 o = make_float4(v.x + acc[q].x, v.y + acc[q].y, v.z + acc[q].z,
+                                           v.w + acc[q].w);
+              const size_t off = static_cast<size_t>(m0 + c0 + r) * args.ldo + col;
+              if (args.out_f32) {
+                *reinterpret_cast<float4*>(reinterpret_cast<float*>(args.out) + off) = o;
+              } else {
+                uint2 packed;
+                packed.x = pack_bf16(o.x, o.y);
+                packed.y = pack_bf16(o.z, o.w);
+                *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(args.out) + off) =
+                    packed;
+              }
+            }
           }
         }
         epi_bar_sync();
       }
-      // the accumulator is drained: release it to the MMA warp before any fix-up work
+      // the accumulator is drained: release it to the MMA warp
       tc_fence_before();
       if (lane == 0) mbar_arrive_cluster(tempty_leader_base + b * 8);
-      if (args.splits > 1) {
-        // last unit of this (tile, CTA half) reduces the partials in split order
+      if (contrib) {  // publish the partial
+        if (tl < 2) GEMM_TRACE(4 * static_cast<int>(tl) + 2);
         __threadfence();
         epi_bar_sync();
-        if (threadIdx.x == 64) {
-          const int prev = atomicAdd(&args.counters[t * 2 + rank], 1);
-          *last_flag = prev == args.splits - 1 ? 1 : 0;
-        }
-        epi_bar_sync();
-        if (*last_flag) {
-          __threadfence();
-          for (int c0 = 0; c0 < rows; c0 += kEpiRows) {
-            const int crow = min(kEpiRows, rows - c0);
-            float4 acc[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int zz = 0; zz < args.splits; ++zz) {  // split order: deterministic sum
-              const float* wz = args.workspace + static_cast<size_t>(zz) * args.M * args.N;
-              float4 v[8];
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {  // 8 independent loads in flight
-                const int r = ew + 4 * q;
-                if (r < crow)
-                  v[q] = __ldcg(reinterpret_cast<const float4*>(
-                      wz + static_cast<size_t>(m0 + c0 + r) * args.N + col));
-              }
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                if (ew + 4 * q < crow) {
-                  acc[q].x += v[q].x;
-                  acc[q].y += v[q].y;
-                  acc[q].z += v[q].z;
-                  acc[q].w += v[q].w;
-                }
-              }
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const int r = ew + 4 * q;
-              if (r < crow) reinterpret_cast<float4*>(staging + r * 128)[lane] = acc[q];
-            }
-            __syncwarp();
-            store_chunk(args, staging, m0 + c0, crow, ew, lane, col);
-            __syncwarp();
-          }
-          if (threadIdx.x == 64) args.counters[t * 2 + rank] = 0;
-        }
-        epi_bar_sync();
+        if (threadIdx.x == 64) st_release_gpu(args.flags + 2 * pair + rank, 1);
+        if (tl < 2) GEMM_TRACE(4 * static_cast<int>(tl) + 3);
+      } else if (head && threadIdx.x == 64) {
+        for (int q = pair + 1; q < q_end; ++q) args.flags[2 * q + rank] = 0;  // consumed
       }
     }
   }
 
+  GEMM_TRACE(13);
   __syncwarp();
   tc_fence_before();
   __syncthreads();
+  GEMM_TRACE(14);
   cluster_sync();
   if (warp == 2) {
     tc_fence_after();
@@ -396,9 +514,10 @@ int32_t launch2(const CUtensorMap* tw, const CUtensorMap* tx, const Gemm2Args& a
       return CORTEX_ECUDA;
     configured = true;
   }
-  const int units = a.num_tiles * a.splits;
-  const int pairs = units < n_sms / 2 ? units : n_sms / 2;
-  kern<<<2 * pairs, kThreads2, L::kTotal, stream>>>(*tw, *tx, a);
+  Gemm2Args b = a;
+  b.npairs = b.sk ? n_sms / 2 : (a.num_tiles < n_sms / 2 ? a.num_tiles : n_sms / 2);
+  if (b.sk && b.total_units < b.npairs) b.npairs = b.total_units;
+  kern<<<2 * b.npairs, kThreads2, L::kTotal, stream>>>(*tw, *tx, b);
   CORTEX_CHECK_LAUNCH();
   return CORTEX_OK;
 }
@@ -407,26 +526,56 @@ int g_num_sms = 0;
 
 }  // namespace
 
-// Tile width (m) and K splits the 2-SM GEMM uses for a problem: fewest waves of
-// work units x (per-unit MMA time + overhead), a split costing ~10 % for its fix-up.
-void cortex_gemm2_plan(int M, int N, int K, int n_sms, int* tn_out, int* splits_out) {
+// Tile width (m) and mode the 2-SM GEMM uses for a problem: the lowest modelled
+// time over TN of whole tiles (waves x (TN + 32)). Stream-K is only used when forced
+// (cortex_gemm_set_stream_k / CORTEX_GEMM_SK=1): it balances the MMA work, but the
+// head pair's fix-up epilogue (reading the partials) measured ~5 us per 32-row chunk
+// at the end of the kernel, so e.g. the down projection at M = 700 takes 107 us vs
+// 73 us in whole tiles (benchmarks/gemm_trace.py with a -DCORTEX_GEMM_TRACE build).
+static int g_sk_force = -2;
+
+int32_t cortex_gemm_set_stream_k(int32_t force) {
+  if (force < -1 || force > 1) return CORTEX_EBADARG;
+  g_sk_force = force;
+  return CORTEX_OK;
+}
+
+void cortex_gemm2_plan(int M, int N, int K, int n_sms, int* tn_out, int* sk_out) {
+  if (g_sk_force == -2) {
+    const char* e = getenv("CORTEX_GEMM_SK");
+    g_sk_force = e ? atoi(e) : -1;
+  }
+  const int force = g_sk_force == 1 ? 1 : 0;
   const int n_tiles = N / kPairN;
   const int pairs = n_sms / 2;
-  const int total_kb = K / kBK;
   double best = -1.0;
   for (int tn : {256, 224, 192, 160, 128, 96, 64}) {
-    for (int sp = 1; sp <= kMaxSplits2; ++sp) {
-      if (sp > 1 && total_kb / sp < 8) break;
-      const long units = static_cast<long>(n_tiles) * ((M + tn - 1) / tn) * sp;
+    const long units = static_cast<long>(n_tiles) * ((M + tn - 1) / tn);
+    for (int sk = 0; sk <= 1; ++sk) {
+      if (force >= 0 && sk != force) continue;
       const long waves = (units + pairs - 1) / pairs;
-      const double cost = waves * (tn + 32.0) / sp * (sp > 1 ? 1.1 : 1.0);
+      const double cost = sk ? static_cast<double>(units) / pairs * (tn + 32.0) * 1.06 + 16.0
+                             : waves * (tn + 32.0);
       if (best < 0 || cost < best - 1e-9) {
         best = cost;
         *tn_out = tn;
-        *splits_out = sp;
+        *sk_out = sk;
       }
     }
   }
+}
+
+int32_t cortex_gemm2_tile(int32_t M, int32_t N, int32_t K) {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        g_num_sms < 2)
+      g_num_sms = 148;
+  }
+  int tn = 256, sk = 0;
+  cortex_gemm2_plan(M, N, K, g_num_sms, &tn, &sk);
+  return tn | (sk << 16);
 }
 
 int32_t cortex_gemm_2sm_launch(const void* tmap_w, const void* tmap_x, int32_t M, int32_t N,
@@ -441,14 +590,14 @@ int32_t cortex_gemm_2sm_launch(const void* tmap_w, const void* tmap_x, int32_t M
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms < 2) g_num_sms = 148;
   }
-  int tn = 256, splits = 1;
-  cortex_gemm2_plan(M, N, K, g_num_sms, &tn, &splits);
+  int tn = 256, sk = 0;
+  cortex_gemm2_plan(M, N, K, g_num_sms, &tn, &sk);
   const int m_tiles = (M + tn - 1) / tn;
   const int num_tiles = (N / kPairN) * m_tiles;
-  if (splits > 1 && (!workspace || !counters ||
-                     workspace_bytes < static_cast<uint64_t>(splits) * M * N * sizeof(float) ||
-                     n_counters < 2 * num_tiles))
-    splits = 1;
+  if (sk && (!workspace || !counters ||
+             workspace_bytes < static_cast<uint64_t>(g_num_sms) * tn * 128 * sizeof(float) ||
+             n_counters < g_num_sms))
+    sk = 0;
   Gemm2Args a{};
   a.M = M;
   a.N = N;
@@ -460,10 +609,10 @@ int32_t cortex_gemm_2sm_launch(const void* tmap_w, const void* tmap_x, int32_t M
   a.ldr = ldr;
   a.m_tiles = m_tiles;
   a.num_tiles = num_tiles;
-  a.splits = splits;
-  a.kb_per_split = (K / kBK + splits - 1) / splits;
+  a.sk = sk;
+  a.total_units = num_tiles * (K / kBK);
   a.workspace = workspace;
-  a.counters = counters;
+  a.flags = counters;
   const auto* tw = reinterpret_cast<const CUtensorMap*>(tmap_w);
   const auto* tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
   switch (tn) {

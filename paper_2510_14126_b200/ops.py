@@ -111,6 +111,11 @@ def gemm_set_mode(mode: int) -> None:
     _check(lib().cortex_gemm_set_mode(mode), "cortex_gemm_set_mode")
 
 
+def gemm_set_stream_k(force: int) -> None:
+    """-1 automatic, 0 whole tiles, 1 stream-K (2-SM kernel scheduling)."""
+    _check(lib().cortex_gemm_set_stream_k(force), "cortex_gemm_set_stream_k")
+
+
 def gemm(wmap: TensorMap, xmap: TensorMap, M: int, out: torch.Tensor, ws: GemmWorkspace,
          residual: torch.Tensor | None = None, swiglu: bool = False, stream=None) -> torch.Tensor:
     """out[:M] = X[:M] @ W^T (+ residual). out is bf16 or fp32 [>=M, N] row-major.

@@ -75,34 +75,42 @@ def test_gemm_residual_and_f32(cuda, M):
     assert rel(out32, x[:M].float() @ w.float().T) < 1e-5
 
 
-@pytest.mark.parametrize("mode", [1, 2])
+def _set_gemm_mode(o, mode):
+    """0 automatic, 1 = 1-SM kernel, 2 = 2-SM whole tiles, 3 = 2-SM stream-K."""
+    o.gemm_set_mode(min(mode, 2))
+    o.gemm_set_stream_k({0: -1, 1: -1, 2: 0, 3: 1}[mode])
+
+
+@pytest.mark.parametrize("mode", [1, 2, 3])
 @pytest.mark.parametrize("M,N,K", [(129, 512, 256), (700, 4096, 4096), (300, 6144, 4096),
                                    (2048, 1536, 256), (33, 1024, 768), (1000, 28672, 4096),
                                    (4096, 4096, 14336), (5, 256, 4096)])
 def test_gemm_paths_match(cuda, mode, M, N, K):
-    """Both kernels (1-SM split-K and persistent 2-SM cta_group::2) on the same problems."""
+    """Both kernels (1-SM split-K and persistent 2-SM cta_group::2, the latter with whole
+    tiles (mode 2) or stream-K ranges (mode 3)) on the same problems."""
     o = ops()
     g = torch.Generator(device=cuda).manual_seed(M + N)
     x = torch.randn(max(M, 32), K, generator=g, device=cuda).to(torch.bfloat16)
     w = (torch.randn(N, K, generator=g, device=cuda) * 0.05).to(torch.bfloat16)
     r = torch.randn(M, N, generator=g, device=cuda)
     ws = o.GemmWorkspace(cuda)
-    o.gemm_set_mode(mode)
+    _set_gemm_mode(o, mode)
     try:
         out = torch.full((M, N), float("nan"), device=cuda, dtype=torch.bfloat16)
         o.gemm(o.weight_map(w), o.act_map(x), M, out, ws)
         out32 = torch.empty(M, N, device=cuda)
         o.gemm(o.weight_map(w), o.act_map(x), M, out32, ws, residual=r)
         torch.cuda.synchronize()
+        assert int(ws.counters.abs().sum()) == 0  # stream-K flags left zeroed
     finally:
-        o.gemm_set_mode(0)
+        _set_gemm_mode(o, 0)
     ref = x[:M].float() @ w.float().T
     assert torch.isfinite(out.float()).all()
     assert rel(out, ref) < 4e-3
     assert rel(out32, ref + r) < 4e-5  # fp32 accumulation order over K <= 14336
 
 
-@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("mode", [1, 2, 3])
 @pytest.mark.parametrize("M,F,K", [(7, 768, 256), (300, 768, 256), (700, 14336, 4096),
                                    (64, 14336, 4096)])
 def test_gemm_fused_swiglu(cuda, mode, M, F, K):
@@ -114,12 +122,12 @@ def test_gemm_fused_swiglu(cuda, mode, M, F, K):
     wi = o.interleave_gate_up(w)
     assert torch.equal(o.deinterleave_gate_up(wi), w)
     out = torch.full((M, F), float("nan"), device=cuda, dtype=torch.bfloat16)
-    o.gemm_set_mode(mode)
+    _set_gemm_mode(o, mode)
     try:
         o.gemm(o.weight_map(wi), o.act_map(x), M, out, o.GemmWorkspace(cuda), swiglu=True)
         torch.cuda.synchronize()
     finally:
-        o.gemm_set_mode(0)
+        _set_gemm_mode(o, 0)
     gu = x[:M].float() @ w.float().T
     gg, uu = gu[:, :F], gu[:, F:]
     ref = gg / (1 + torch.exp(-gg)) * uu
