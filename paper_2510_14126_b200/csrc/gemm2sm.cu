@@ -516,6 +516,9 @@ int32_t launch2(const CUtensorMap* tw, const CUtensorMap* tx, const Gemm2Args& a
   }
   Gemm2Args b = a;
   b.npairs = b.sk ? n_sms / 2 : (a.num_tiles < n_sms / 2 ? a.num_tiles : n_sms / 2);
+#ifdef CORTEX_GEMM_MAXPAIRS  // (tuning experiment: fewer concurrent pairs)
+  if (b.npairs > CORTEX_GEMM_MAXPAIRS) b.npairs = CORTEX_GEMM_MAXPAIRS;
+#endif
   if (b.sk && b.total_units < b.npairs) b.npairs = b.total_units;
   kern<<<2 * b.npairs, kThreads2, L::kTotal, stream>>>(*tw, *tx, b);
   CORTEX_CHECK_LAUNCH();
