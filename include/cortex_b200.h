@@ -41,7 +41,8 @@ enum {
   CORTEX_EBADARG = -1,
   CORTEX_ECUDA = -2,
   CORTEX_ENOBLOCKS = -3,
-  CORTEX_EUNSUPPORTED = -4
+  CORTEX_EUNSUPPORTED = -4,
+  CORTEX_ETIMEOUT = -5 /* a cross-GPU wait exceeded its bound (peer rank gone) */
 };
 
 /* ABI version (major * 100 + minor). */
@@ -229,6 +230,35 @@ int32_t cortex_paged_prefill_attn(const void* tmap_kv, const void* q, void* out,
                                   const int32_t* seq_qlen, int32_t n_seqs, int32_t max_qlen,
                                   int32_t n_kv_heads, int32_t group, int64_t k_row0,
                                   int64_t v_row0, float softmax_scale, cortex_stream_t stream);
+
+/* ---- Tensor parallelism (TP = 2 inside one engine replica, BASELINE config 5) -------
+ * the only collective on the path. The reference engine has no
+ * model and hence no TP (engines.py:101-246); these exports implement the
+ * all-reduce of the O / down projection partials that a TP = 2 replica of the
+ * decoder forward (the GPU half of EngineState.advance_decode / admit) needs.
+ *
+ * cortex_sym_alloc: zeroed device buffer [flags (cortex_tp_flag_bytes()) | partial
+ * parity 0 | partial parity 1], shareable with the peer rank through CUDA IPC
+ * (cortex_ipc_get_handle -> 64-byte handle -> cortex_ipc_open_handle in the peer).
+ * cortex_tp_signal: after the stream's preceding work (the partial-output GEMM),
+ * publish `epoch` into the peer's flag word (system-scope release).
+ * cortex_tp_allreduce_rmsnorm: wait until *flag >= epoch (system-scope acquire;
+ * CORTEX_ETIMEOUT into *status after 10 s), then for each of n_rows rows
+ * x += y0 + y1 (rank 0's partial first: bit-identical residuals on both ranks) and,
+ * when w != NULL, out = bf16(x * rsqrt(mean(x^2) + eps) * w). y0 / y1 may be peer
+ * (NVLink) pointers. flag == NULL skips the wait.
+ */
+int32_t cortex_sym_alloc(uint64_t bytes, void** out_ptr);
+int32_t cortex_sym_free(void* ptr);
+int32_t cortex_ipc_get_handle(void* ptr, void* handle_out /* 64 bytes */);
+int32_t cortex_ipc_open_handle(const void* handle, void** out_ptr);
+int32_t cortex_ipc_close(void* ptr);
+int32_t cortex_tp_flag_bytes(void);
+int32_t cortex_tp_signal(uint32_t* peer_flag, uint32_t epoch, cortex_stream_t stream);
+int32_t cortex_tp_allreduce_rmsnorm(const float* y0, const float* y1, float* x, int32_t n_rows,
+                                    int32_t d, const void* w, float eps, void* out,
+                                    const uint32_t* flag, uint32_t epoch, int32_t* status,
+                                    cortex_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -53,10 +53,19 @@ SIGNATURES: dict[str, list] = {
                                P, P, I32, P],
     "cortex_paged_prefill_attn": [P, P, P, P, I32, P, P, P, P, P, I32, I32, I32, I32, I64, I64,
                                   F32, P],
+    "cortex_sym_alloc": [U64, P],
+    "cortex_sym_free": [P],
+    "cortex_ipc_get_handle": [P, P],
+    "cortex_ipc_open_handle": [P, P],
+    "cortex_ipc_close": [P],
+    "cortex_tp_flag_bytes": [],
+    "cortex_tp_signal": [P, ctypes.c_uint32, P],
+    "cortex_tp_allreduce_rmsnorm": [P, P, P, I32, I32, P, F32, P, P, ctypes.c_uint32, P, P],
 }
 
 STATUS_NAMES = {0: "ok", -1: "bad argument", -2: "CUDA error", -3: "out of KV blocks",
-                -4: "unsupported"}
+                -4: "unsupported",
+                -5: "cross-GPU wait timed out"}
 
 _LIB: ctypes.CDLL | None = None
 

@@ -60,8 +60,13 @@ class ModelConfig:
 TINY = ModelConfig("tiny-4L-d256", n_layers=4, d_model=256, n_heads=2, n_kv_heads=1, ffn=768,
                    vocab=1024, rope_theta=10000.0)
 
+# Tiny shape that splits two ways (BASELINE config 5 is tensor-parallel = 2): 4 q heads
+# over 2 kv heads, so each TP rank keeps one whole GQA group of head_dim 128.
+TINY_TP = ModelConfig("tiny-tp-4L-d256", n_layers=4, d_model=256, n_heads=4, n_kv_heads=2,
+                      ffn=768, vocab=1024, rope_theta=10000.0)
+
 # BASELINE configs 2-5: Llama-3-8B shape (random init).
 LLAMA3_8B = ModelConfig("llama3-8b", n_layers=32, d_model=4096, n_heads=32, n_kv_heads=8,
                         ffn=14336, vocab=128256, rope_theta=500000.0)
 
-MODELS = {m.name: m for m in (TINY, LLAMA3_8B)}
+MODELS = {m.name: m for m in (TINY, TINY_TP, LLAMA3_8B)}

@@ -143,7 +143,20 @@ class GpuWorker:
 
     def __init__(self, cfg: ModelConfig, device, n_blocks: int, n_rows: int, row_cols: int,
                  max_tokens: int = 4096, max_out: int = 512, hist_cols: int = 1024,
-                 max_seq_tokens: int = 16384, weights: dict | None = None, seed: int = 0) -> None:
+                 max_seq_tokens: int = 16384, weights: dict | None = None, seed: int = 0,
+                 tp=None) -> None:
+        # tp: a tp.TpComm when this worker is one rank of a TP = 2 replica. `cfg` is the
+        # full model; the worker holds its rank's shard (tp.py) and self.cfg is the shard.
+        self.full_cfg = cfg
+        self.tp = tp
+        if tp is not None:
+            from .tp import shard_config, shard_weights
+
+            if tp.max_tokens < max_tokens or tp.d != cfg.d_model:
+                raise ValueError("TpComm buffer smaller than the worker's step")
+            full = weights if weights is not None else init_weights(cfg, device, seed)
+            weights = shard_weights(full, cfg, tp.rank, tp.size)
+            cfg = shard_config(cfg, tp.size)
         self.cfg = cfg
         self.device = torch.device(device)
         self.n_blocks = n_blocks
@@ -306,11 +319,22 @@ class GpuWorker:
     @torch.no_grad()
     def forward(self, plan: StepPlan) -> int:
         """Run one batched step; returns the number of greedy tokens produced."""
+        for _ in self.forward_steps(plan):
+            pass
+        return self.n_out
+
+    @torch.no_grad()
+    def forward_steps(self, plan: StepPlan):
+        """forward() as a generator that yields at every TP exchange point (after the
+        partial-output GEMM and its signal were enqueued, before the reduce that reads
+        the peer's partial); a TP = 1 worker never yields. The result is left in
+        self.n_out."""
         cfg = self.cfg
         n_dec = len(plan.decode)
         T = plan.n_tokens
+        self.n_out = 0
         if T == 0:
-            return 0
+            return
         if T > self.max_tokens:
             raise ValueError(f"step of {T} tokens exceeds max_tokens={self.max_tokens}")
         i32 = np.int32
@@ -448,14 +472,17 @@ class GpuWorker:
                 prof.close("gemm", e0, 2.0 * N * K + 2.0 * M * K + ob * M * n_out,
                            2.0 * M * N * K)
 
+        tp = self.tp
         for li in range(cfg.n_layers):
             p = f"layers.{li}."
             k0, v0 = self.layer_rows(li)
-            ops.rmsnorm(x, w[p + "attn_norm"], T, xn, cfg.eps)
+            if tp is None or li == 0:  # TP: fused into the previous layer's down exchange
+                ops.rmsnorm(x, w[p + "attn_norm"], T, xn, cfg.eps)
+                nl += 1
             gemm(p + "wqkv", self.xn_map, T, self.qkv)
             ops.rope_kv_append(self.qkv, self.q, self.cache, k0, v0, self.table, d_pos, d_arow,
                                d_acol, d_aoff, self.cos, self.sin, T, hq, hkv)
-            nl += 3
+            nl += 2
             def prefill_attn(stream=None):
                 if self.tc_attention:
                     ops.fmha_prefill(self.kvmap, self.qmap, self.attn, self.table, d_prow, d_ppre,
@@ -504,11 +531,28 @@ class GpuWorker:
                 if e0 is not None:
                     prof.close("attn_prefill", e0, pf_bytes, pf_flops)
                 nl += 1
-            gemm(p + "wo", self.attn_map, T, x, residual=x)
-            ops.rmsnorm(x, w[p + "mlp_norm"], T, xn, cfg.eps)
+            if tp is None:
+                gemm(p + "wo", self.attn_map, T, x, residual=x)
+                ops.rmsnorm(x, w[p + "mlp_norm"], T, xn, cfg.eps)
+                nl += 2
+            else:  # partial O -> [peer exchange + residual + mlp_norm] (csrc/tp.cu)
+                gemm(p + "wo", self.attn_map, T, tp.out())
+                tp.signal()
+                yield li
+                tp.reduce(x, T, w[p + "mlp_norm"], cfg.eps, xn)
+                nl += 3
             gemm(p + "wgu", self.xn_map, T, self.act, swiglu=True)  # SwiGLU in the epilogue
-            gemm(p + "wd", self.act_map, T, x, residual=x)
-            nl += 5
+            nl += 1
+            if tp is None:
+                gemm(p + "wd", self.act_map, T, x, residual=x)
+                nl += 1
+            else:  # partial down -> [exchange + residual + next layer's attn_norm]
+                gemm(p + "wd", self.act_map, T, tp.out())
+                tp.signal()
+                yield li
+                nxt = f"layers.{li + 1}.attn_norm"
+                tp.reduce(x, T, w.get(nxt), cfg.eps, xn if nxt in w else None)
+                nl += 3
         if n_out:
             ops.rmsnorm(x, w["final_norm"], n_out, self.xn_out, cfg.eps, rows=d_orow)
             gemm("lm_head", self.xn_out_map, n_out, self.logits)
@@ -517,6 +561,6 @@ class GpuWorker:
             nl += 3
         self.launches += nl
         self.steps += 1
+        self.n_out = n_out
         if self.on_forward is not None:
             self.on_forward(plan, n_out)
-        return n_out

@@ -1,0 +1,150 @@
+"""TP = 2 replica of the decoder forward (tp.py, csrc/tp.cu) on one B200.
+
+1. In-process: the two ranks of a replica live on cuda:0 with their own symmetric
+   buffers, driven in lockstep (tp.lockstep) so every exchange wait is already
+   satisfied by stream order. Checks: both ranks' residual streams and logits are
+   bit-identical, the logits match the CPU fp32 decoder oracle within the north
+   star's bf16 tolerance (2e-3 relative), greedy tokens equal the oracle's (near-ties
+   excepted), and the TP = 1 worker on the same weights agrees.
+2. Two processes on the same GPU, peers mapped through CUDA IPC, a host barrier at
+   every exchange point (so no kernel waits on the other process): exercises the
+   IPC mapping and the system-scope signal path; results must equal run 1 bit for bit.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+import tp_script
+from oracle.decoder_ref import RefDecoder, greedy, top2_margin
+from paper_2510_14126_b200.config import TINY_TP
+from paper_2510_14126_b200.model import init_weights
+from paper_2510_14126_b200.tp import TpComm, shard_config
+
+pytestmark = pytest.mark.gpu
+
+LOGIT_TOL = 2e-3
+TIE_TOL = 2e-2
+
+
+def _full_weights(device):
+    return init_weights(TINY_TP, device, seed=3)
+
+
+def _pair(device, weights):
+    comms = [TpComm(device, r, 2, tp_script.MAX_TOKENS, TINY_TP.d_model) for r in (0, 1)]
+    TpComm.connect_local(*comms)
+    workers = [tp_script.make_worker(TINY_TP, device, weights, tp=c) for c in comms]
+    return comms, workers
+
+
+def _rel(a: torch.Tensor, b: torch.Tensor) -> float:
+    a, b = a.double().cpu(), b.double().cpu()
+    return float((a - b).norm() / b.norm())
+
+
+def test_tp2_lockstep_parity(cuda):
+    full = _full_weights(cuda)
+    canon = {k: v.clone() for k, v in full.items()}
+    comms, workers = _pair(cuda, full)
+    assert workers[0].cfg == shard_config(TINY_TP, 2)
+    assert workers[0].cache.shape[3] == TINY_TP.n_kv_heads // 2
+    logs = tp_script.run_lockstep(workers, TINY_TP.vocab)
+    torch.cuda.synchronize()
+    for c in comms:
+        assert int(c.status[0]) == 0
+    for w in workers:
+        assert int(w.status[0]) == 0
+    # the two ranks agree bit for bit (fixed-order reduction of the partials)
+    assert torch.equal(workers[0].x, workers[1].x)
+    for a, b in zip(*logs):
+        assert torch.equal(a, b)
+    assert torch.equal(workers[0].hist, workers[1].hist)
+    # TP = 1 on the same weights (the same step script)
+    ref = tp_script.make_worker(TINY_TP, cuda, {k: v.clone() for k, v in canon.items()})
+    ref_logs = tp_script.run_lockstep([ref], TINY_TP.vocab)
+    torch.cuda.synchronize()
+    first = [_rel(a, b) for a, b in zip(logs[0], ref_logs[0])]
+    assert first[0] < 1e-3, first  # the first step has identical inputs
+    # CPU fp32 oracle, teacher-forced on the TP replica's own greedy tokens
+    dec = RefDecoder(TINY_TP.to_ref(), {k: v.float().cpu() for k, v in canon.items()},
+                     max_pos=tp_script.MAX_SEQ)
+    hist = workers[0].hist.cpu().numpy()
+    prompts = tp_script.prompts(TINY_TP.vocab)
+    # row r's logits per step: (step, index within the step's output rows)
+    where = {0: [(0, 0)] + [(1 + k, 0) for k in range(tp_script.DECODE_STEPS + 1)],
+             1: [(1, 1)] + [(2 + k, 1) for k in range(tp_script.DECODE_STEPS)]}
+    worst, flips, n_tok = 0.0, 0, 0
+    for row in (0, 1):
+        seq = dec.new_seq()
+        lg = seq.extend(prompts[row])
+        for k, (st, j) in enumerate(where[row]):
+            if k:
+                lg = seq.extend([int(hist[row, k - 1])])
+            got = logs[0][st][j]
+            worst = max(worst, _rel(got, lg.reshape(-1)))
+            n_tok += 1
+            if greedy(lg) != int(hist[row, k]):
+                flips += 1
+                assert top2_margin(lg) < TIE_TOL, (row, k)
+    print(f"\nTP=2 lockstep: {n_tok} positions, worst logit rel err {worst:.2e}, "
+          f"{flips} near-tie flips")
+    assert worst < LOGIT_TOL
+    assert flips <= 1
+    for c in comms:
+        c.close()
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _ipc_rank(rank: int, port: int, out_dir: str) -> None:
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    comm = TpComm(dev, rank, 2, tp_script.MAX_TOKENS, TINY_TP.d_model)
+    comm.connect_ipc()
+    w = tp_script.make_worker(TINY_TP, dev, _full_weights(dev), tp=comm)
+
+    def between():  # both ranks' partial + signal complete before either reduces
+        torch.cuda.synchronize()
+        dist.barrier()
+
+    logs = tp_script.run_lockstep([w], TINY_TP.vocab, between=between)
+    torch.cuda.synchronize()
+    torch.save({"logits": [t.cpu() for t in logs[0]], "x": w.x.cpu(), "hist": w.hist.cpu(),
+                "status": int(comm.status[0]) | int(w.status[0])},
+               os.path.join(out_dir, f"rank{rank}.pt"))
+    dist.barrier()
+    comm.close()
+    dist.destroy_process_group()
+
+
+def test_tp2_two_processes_ipc(cuda, tmp_path):
+    import torch.multiprocessing as mp
+
+    comms, workers = _pair(cuda, _full_weights(cuda))
+    logs = tp_script.run_lockstep(workers, TINY_TP.vocab)
+    torch.cuda.synchronize()
+    mp.start_processes(_ipc_rank, args=(_free_port(), str(tmp_path)), nprocs=2, join=True,
+                       start_method="spawn")
+    res = [torch.load(tmp_path / f"rank{r}.pt") for r in (0, 1)]
+    for r in (0, 1):
+        assert res[r]["status"] == 0
+        assert torch.equal(res[r]["x"], workers[r].x.cpu())
+        assert torch.equal(res[r]["hist"], workers[r].hist.cpu())
+        for a, b in zip(res[r]["logits"], logs[r]):
+            assert torch.equal(a, b.cpu())
+    for c in comms:
+        c.close()
