@@ -105,18 +105,21 @@ def workload(name: str):
         return Nl2Sql(retry_budget=5, generator_prefix_tokens=8192, fixer_prefix_tokens=8192,
                       output_tokens=Constant(512)), \
             "config4: NL2SQL isolated, 8K schema prefix, 512-token outputs, budget 5, seed 0"
+    if name == "config5":
+        return Nl2Sql(retry_budget=5, p_fail=0.6, p_syntax_err=0.3, p_empty_result=0.3), \
+            "config5: NL2SQL isolated, heavy retry (p_fail 0.6 = 0.3 syntax + 0.3 empty), " \
+            "budget 5, seed 0"
     raise ValueError(name)
 
 
-def build_runtime(model_name: str, wl_name: str, concurrency: int, device, rank: int, world: int,
-                  max_tokens: int = 4096, role: str = "both", channel=None):
+def build_worker(model_name: str, spec, concurrency: int, device, role: str = "both",
+                 max_tokens: int = 4096, tp_comm=None):
+    """The GPU worker (weights, KV arena) sized for `concurrency` calls per engine."""
     from paper_2510_14126_b200.config import MODELS
     from paper_2510_14126_b200.engine import EngineParams, blocks_for
     from paper_2510_14126_b200.model import GpuWorker
-    from paper_2510_14126_b200.runtime import PoolRuntime
 
     cfg = MODELS[model_name]
-    spec, desc = workload(wl_name)
     P = max(spec.generator_prefix_tokens, spec.fixer_prefix_tokens)
     p_hi = int(spec.prompt_tokens.high)
     o_hi = int(getattr(spec.output_tokens, "high", getattr(spec.output_tokens, "value", 0)))
@@ -129,7 +132,24 @@ def build_runtime(model_name: str, wl_name: str, concurrency: int, device, rank:
     worker = GpuWorker(cfg, device, n_blocks=n_eng * bpe, n_rows=n_eng * (concurrency + 4),
                        row_cols=(max_seq + 15) // 16 + 2, max_tokens=max_tokens,
                        max_out=2 * concurrency + 64, hist_cols=o_hi + 8,
-                       max_seq_tokens=max_seq + 16, seed=0)
+                       max_seq_tokens=max_seq + 16, seed=0, tp=tp_comm)
+    return worker, params
+
+
+def build_runtime(model_name: str, wl_name: str, concurrency: int, device, rank: int, world: int,
+                  max_tokens: int = 4096, role: str = "both", channel=None, tp_comm=None,
+                  tp_ring=None):
+    """rank / world: replica index and count. tp_comm + tp_ring: this rank leads a TP = 2
+    replica (its worker is wrapped so the follower rank mirrors every device call)."""
+    from paper_2510_14126_b200.runtime import PoolRuntime
+    from paper_2510_14126_b200.tp import TpLeader
+
+    spec, desc = workload(wl_name)
+    worker, params = build_worker(model_name, spec, concurrency, device, role, max_tokens,
+                                  tp_comm)
+    cfg = worker.full_cfg
+    if tp_ring is not None:
+        worker = TpLeader(worker, tp_ring)
     if role == "both":  # replicas: workflows interleaved by rank
         rid_offset, rid_stride = rank, world
     else:  # disjoint pairs: workflows interleaved by pair
@@ -164,6 +184,9 @@ def main() -> None:
     ap.add_argument("--placement", default="disjoint", choices=["disjoint", "replicas"],
                     help="N>1: generator and fixer pools on disjoint GPUs (pairs), or "
                          "both pools on every GPU")
+    ap.add_argument("--tp", type=int, default=1, choices=[1, 2],
+                    help="tensor-parallel size of each engine replica (config 5: 2); "
+                         "replicas are rank pairs (2i, 2i+1), placement applies to replicas")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -211,13 +234,54 @@ def main() -> None:
     from paper_2510_14126_b200.model import KernelProfile
     from paper_2510_14126_b200.placement import ROLE_BOTH, ROLE_FIXER, open_pair_channel, role_of
 
-    role, pair, _ = role_of(rank, world) if args.placement == "disjoint" else (ROLE_BOTH, rank, -1)
+    # TP = 2: ranks (2i, 2i+1) form replica i; rank 2i leads (runs the runtime), 2i+1 follows
+    tp = args.tp
+    if world % tp:
+        raise SystemExit("--tp must divide the number of ranks")
+    rrank, rworld, tp_rank = rank // tp, world // tp, rank % tp
+    role, pair, _ = (role_of(rrank, rworld) if args.placement == "disjoint"
+                     else (ROLE_BOTH, rrank, -1))
     # per-GPU load is fixed as N grows: a disjoint pair (2 GPUs) carries 2x the workflows
     conc = args.concurrency * (2 if role != ROLE_BOTH else 1)
-    channel = open_pair_channel(dist, rank, world, cap=2 * conc + 64) if role != ROLE_BOTH else None
-    rt, cfg, desc = build_runtime(args.model, args.workload, conc, device, rank, world,
-                                  role=role, channel=channel)
+    channel = (open_pair_channel(dist, rrank, rworld, cap=2 * conc + 64, member=tp_rank == 0)
+               if role != ROLE_BOTH else None)
+    tp_comm = tp_ring = None
+    if tp > 1:
+        from paper_2510_14126_b200.config import MODELS
+        from paper_2510_14126_b200.tp import TpComm, open_replica_ring
+
+        groups = [dist.new_group([tp * i + j for j in range(tp)]) for i in range(rworld)]
+        tp_comm = TpComm(device, tp_rank, tp, 4096, MODELS[args.model].d_model)
+        tp_comm.connect_ipc(groups[rrank])
+        tp_ring = open_replica_ring(dist, rrank, tp_rank)
+        if os.environ.get("CORTEX_TP_HOST_SYNC") == "1":
+            # functional runs with a replica's two ranks on ONE GPU (gloo): every exchange
+            # waits on the host until both ranks' partials exist (no cross-rank spinning)
+            def host_sync(g=groups[rrank]):
+                torch.cuda.synchronize()
+                dist.barrier(group=g)
+            tp_sync = host_sync
+        else:
+            tp_sync = None
+        if tp_rank:
+            _follow(args, device, role, conc, tp_comm, tp_ring, dist, comm_dev, tp_sync)
+            return
+    rt, cfg, desc = build_runtime(args.model, args.workload, conc, device, rrank, rworld,
+                                  role=role, channel=channel, tp_comm=tp_comm, tp_ring=tp_ring)
     w = rt.worker
+    if tp > 1:
+        w.tp_sync = tp_sync
+
+    def coll_barrier() -> None:
+        if tp_ring is not None:
+            w.collective("barrier")
+        dist.barrier()
+
+    def coll_all_reduce(t, op) -> None:
+        if tp_ring is not None:
+            w.collective("all_reduce", t.numel(), str(t.dtype), op)
+        dist.all_reduce(t, op=op)
+
     rt.fill()
 
     def run_phase(n_steps: int, phase: int) -> None:
@@ -233,7 +297,7 @@ def main() -> None:
 
     run_phase(max(3, args.warmup), 0)
     if dist is not None:
-        dist.barrier()
+        coll_barrier()
 
     # kernel-class shares (untimed) -> the dominant kernel for the roofline
     w.prof = KernelProfile(["gemm", "attn_decode", "attn_prefill"])
@@ -254,7 +318,7 @@ def main() -> None:
     w.prof = KernelProfile([dominant], every=8) if args.roofline_window == "timed" else None
     clocks = ClockSampler(local)
     if dist is not None:
-        dist.barrier()
+        coll_barrier()
     torch.cuda.synchronize()
     s0 = (rt.stats.completed, rt.stats.failed, rt.stats.decode_tokens, rt.stats.prefill_tokens,
           rt.stats.steps, w.launches, w.h2d_bytes, rt.stats.d2h_bytes)
@@ -282,7 +346,7 @@ def main() -> None:
     ms = ev0.elapsed_time(ev1)
     if dist is not None:
         t = torch.tensor([ms, t_wall * 1e3], device=comm_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        coll_all_reduce(t, dist.ReduceOp.MAX)
         ms, t_wall = float(t[0]), float(t[1]) / 1e3
     s1 = (rt.stats.completed, rt.stats.failed, rt.stats.decode_tokens, rt.stats.prefill_tokens,
           rt.stats.steps, w.launches, w.h2d_bytes, rt.stats.d2h_bytes)
@@ -291,7 +355,7 @@ def main() -> None:
     if dist is not None:
         t = torch.tensor([completed, failed, dec_tok, pf_tok], device=comm_dev,
                          dtype=torch.float64)
-        dist.all_reduce(t)
+        coll_all_reduce(t, dist.ReduceOp.SUM)
         completed, failed, dec_tok, pf_tok = [float(x) for x in t]
     if args.roofline_window != "timed":
         w.prof = KernelProfile([dominant])
@@ -307,11 +371,11 @@ def main() -> None:
             shares["gemm"]["flops"] / max(shares["gemm"]["bytes"], 1) > 200:
         bound, unit, peak = "tensor", "TFLOP/s", peaks["bf16_tflops_sustained"]
         per_launch = kshare["flops"] / max(kshare["launches"], 1)
-        achieved = kshare["flops"] / (kshare["ms"] / 1e3) / 1e12
+        achieved = kshare["flops"] / max(kshare["ms"] / 1e3, 1e-12) / 1e12
     else:
         bound, unit, peak = "hbm", "GB/s", peaks["hbm_gbs"]
         per_launch = kshare["bytes"] / max(kshare["launches"], 1)
-        achieved = kshare["bytes"] / (kshare["ms"] / 1e3) / 1e9
+        achieved = kshare["bytes"] / max(kshare["ms"] / 1e3, 1e-12) / 1e9
     roofline = {"kernel": dominant, "bound": bound, "achieved": achieved, "peak": peak,
                 "unit": unit, "frac": achieved / peak, "traffic": None,
                 "per_launch_algorithmic": per_launch, "avg_launch_ms": kshare["ms"] / max(
@@ -333,10 +397,13 @@ def main() -> None:
         "dtype": "bf16",
         "data": "synthetic: seeded NL2SQL trace (reference counter streams), random-init weights",
         "config": {"workload": desc, "model": cfg.name + "-shape", "concurrency": args.concurrency,
-                   "engines": "isolated: 1 generator + 1 fixer engine per GPU" if role == ROLE_BOTH
-                   else f"isolated, disjoint placement: GPUs 0..{world // 2 - 1} generator pool, "
-                        f"{world // 2}..{world - 1} fixer pool; {world // 2} pair(s) of "
-                        f"{conc} workflows (host handoff, no collective)",
+                   "engines": ("isolated: 1 generator + 1 fixer engine per replica"
+                               if role == ROLE_BOTH
+                               else f"isolated, disjoint placement: replicas 0..{rworld // 2 - 1} "
+                                    f"generator pool, {rworld // 2}..{rworld - 1} fixer pool; "
+                                    f"{rworld // 2} pair(s) of {conc} workflows (host handoff)")
+                   + (f"; {rworld} replica(s) of TP=2 (GPU pairs, fused NVLink all-reduce)"
+                      if tp > 1 else ""),
                    "l2": "inputs larger than L2 (16 GB of weights + KV streamed every step)"},
         "decode_tok_s": dec_tok / secs,
         "prefill_tok_s": pf_tok / secs,
@@ -358,10 +425,43 @@ def main() -> None:
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
+        if tp_ring is not None:
+            w.stop()
         dist.barrier()
         if channel is not None:
             channel.close()
+        if tp_ring is not None:
+            tp_ring.close()
         dist.destroy_process_group()
+
+
+def _follow(args, device, role, conc, tp_comm, tp_ring, dist, comm_dev, tp_sync=None) -> None:
+    """TP follower rank: build the other half of the replica's worker and replay the
+    leader's device calls until it stops; join the leader's collectives with zeros."""
+    from paper_2510_14126_b200.tp import TpFollower
+
+    spec, _ = workload(args.workload)
+    worker, _ = build_worker(args.model, spec, conc, device, role, tp_comm=tp_comm)
+    worker.tp_sync = tp_sync
+
+    def on_collective(kind, a) -> None:
+        if kind == "barrier":
+            dist.barrier()
+        elif kind == "all_reduce":
+            n, dtype, op = a
+            dist.all_reduce(torch.zeros(n, dtype=getattr(torch, dtype.split(".")[-1]),
+                                        device=comm_dev), op=op)
+        else:
+            raise ValueError(kind)
+
+    TpFollower(worker, tp_ring, on_collective=on_collective).serve()
+    torch.cuda.synchronize()
+    if int(tp_comm.status[0]) or int(worker.status[0]):
+        raise SystemExit("TP follower: device status error")
+    dist.barrier()
+    tp_ring.close()
+    dist.destroy_process_group()
+
 
 
 def _kv_snapshot(rt):

@@ -219,6 +219,9 @@ class GpuWorker:
         self.launches = 0  # kernels of this library launched since construction
         self.steps = 0
         self.on_forward = None  # optional hook(plan, n_out) for parity checking
+        # TP: optional host hook at every exchange point (device sync + a host barrier) so
+        # that two ranks sharing one GPU never have a kernel waiting on the other rank
+        self.tp_sync = None
         self.prof: KernelProfile | None = None  # optional per-kernel-class CUDA-event timing
         self.cascade = True  # shared-prefix decode attention (prefix KV read once per step)
         # tcgen05 flash attention for prefill + the cascade pass (CORTEX_TC_ATTN=0: mma.sync)
@@ -320,7 +323,8 @@ class GpuWorker:
     def forward(self, plan: StepPlan) -> int:
         """Run one batched step; returns the number of greedy tokens produced."""
         for _ in self.forward_steps(plan):
-            pass
+            if self.tp_sync is not None:  # functional TP runs with both ranks on one GPU
+                self.tp_sync()
         return self.n_out
 
     @torch.no_grad()

@@ -133,11 +133,14 @@ def channel_name(tag: str, pair: int) -> str:
     return f"cortex_{tag}_{pair}"
 
 
-def open_pair_channel(dist, rank: int, world: int, cap: int, tag: str | None = None):
+def open_pair_channel(dist, rank: int, world: int, cap: int, tag: str | None = None,
+                      member: bool = True):
     """Create (generator side) / attach (fixer side) this rank's pair channel.
 
-    Collective over the default process group: the generator ranks create their
-    segments, a barrier orders creation before attachment."""
+    rank / world index the engine replicas (= processes unless replicas are TP
+    groups). Collective over the default process group: the generator ranks create
+    their segments, a barrier orders creation before attachment. member=False (a TP
+    follower rank) joins the collectives without opening a channel."""
     role, pair, _ = role_of(rank, world)
     if role == ROLE_BOTH:
         return None
@@ -146,9 +149,9 @@ def open_pair_channel(dist, rank: int, world: int, cap: int, tag: str | None = N
         dist.broadcast_object_list(obj, src=0)
         tag = obj[0]
     ch = PairChannel(channel_name(tag, pair), create=True, cap=cap) \
-        if role == ROLE_GENERATOR else None
+        if role == ROLE_GENERATOR and member else None
     dist.barrier()
-    if ch is None:
+    if ch is None and member:
         ch = PairChannel(channel_name(tag, pair), create=False, cap=cap)
     dist.barrier()
     return ch

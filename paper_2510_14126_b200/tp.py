@@ -28,6 +28,8 @@ drives them in lockstep, see `lockstep`) or across processes by CUDA IPC
 from __future__ import annotations
 
 import ctypes
+import os
+import pickle
 from dataclasses import replace
 
 import torch
@@ -186,3 +188,231 @@ def lockstep(gens) -> None:
             except StopIteration:
                 pass
         live = nxt
+
+
+# ---------------------------------------------------------------------------- replica host side
+#
+# One process per GPU: the replica's rank 0 (the LEADER) runs the runtime - scheduling,
+# admission, routing, workflows - exactly as a TP = 1 engine; rank 1 (the FOLLOWER) holds
+# the other half of the weights and KV heads and only replays the leader's device calls
+# (block allocation / free / table copies and every forward), in the same order, so its
+# block pool, tables and kernels mirror the leader's. The calls cross in a shared-memory
+# byte ring (both ranks of a replica live on one node), one message per forward.
+
+
+class ByteRing:
+    """Single-producer / single-consumer ring of length-prefixed byte messages in a
+    memory-mapped /dev/shm file. The producer writes the payload, then publishes it
+    by advancing the tail (x86 store order keeps them in that order)."""
+
+    HDR = 128  # bytes: head (consumer) at 0, tail (producer) at 64
+
+    def __init__(self, path: str, create: bool, cap: int = 1 << 24) -> None:
+        import numpy as np
+
+        self.path, self.owner, self.cap = path, create, cap
+        if create:
+            with open(path, "wb") as f:
+                f.truncate(self.HDR + cap)
+        self.mm = np.memmap(path, dtype=np.uint8, mode="r+", shape=(self.HDR + cap,))
+        self.ctl = self.mm[:self.HDR].view(np.int64)
+        self.data = self.mm[self.HDR:]
+
+    def _write(self, pos: int, b) -> None:
+        import numpy as np
+
+        arr = np.frombuffer(b, dtype=np.uint8)
+        i = pos % self.cap
+        k = min(len(arr), self.cap - i)
+        self.data[i:i + k] = arr[:k]
+        if k < len(arr):
+            self.data[:len(arr) - k] = arr[k:]
+
+    def _read(self, pos: int, n: int) -> bytes:
+        i = pos % self.cap
+        k = min(n, self.cap - i)
+        if k == n:
+            return self.data[i:i + n].tobytes()
+        return self.data[i:i + k].tobytes() + self.data[:n - k].tobytes()
+
+    def send(self, payload: bytes, timeout: float = 60.0) -> None:
+        import struct
+        import time
+
+        n = 8 + len(payload)
+        if n > self.cap:
+            raise ValueError("message larger than the ring")
+        tail = int(self.ctl[8])
+        t_end = time.perf_counter() + timeout
+        while tail + n - int(self.ctl[0]) > self.cap:
+            if time.perf_counter() > t_end:
+                raise TimeoutError("TP follower stopped draining its ring")
+            time.sleep(0)
+        self._write(tail, struct.pack("<q", len(payload)))
+        self._write(tail + 8, payload)
+        self.ctl[8] = tail + n
+
+    def recv(self) -> bytes | None:
+        import struct
+
+        head = int(self.ctl[0])
+        if int(self.ctl[8]) == head:
+            return None
+        (m,) = struct.unpack("<q", self._read(head, 8))
+        out = self._read(head + 8, m)
+        self.ctl[0] = head + 8 + m
+        return out
+
+    def close(self) -> None:
+        self.mm = self.ctl = self.data = None
+        if self.owner:
+            try:
+                os.unlink(self.path)
+            except FileNotFoundError:
+                pass
+
+
+class TpLeader:
+    """Stands in for the leader's GpuWorker: every device-mutating call is applied
+    locally and recorded for the follower; a forward flushes the record first, so the
+    follower launches the same step while the leader does."""
+
+    def __init__(self, worker, ring: ByteRing) -> None:
+        object.__setattr__(self, "_w", worker)
+        object.__setattr__(self, "_ring", ring)
+        object.__setattr__(self, "_out", [])
+
+    def __getattr__(self, name):
+        return getattr(self._w, name)
+
+    def __setattr__(self, name, value) -> None:
+        setattr(self._w, name, value)
+
+    def _rec(self, *op) -> None:
+        self._out.append(op)
+
+    def flush(self) -> None:
+        if self._out:
+            self._ring.send(pickle.dumps(self._out, protocol=5))
+            self._out.clear()
+
+    def alloc_blocks(self, pool, reqs) -> None:
+        self._rec("alloc_blocks", (pool.block_base, pool.n_blocks), list(reqs))
+        self._w.alloc_blocks(pool, reqs)
+
+    def free_blocks(self, pool, reqs) -> None:
+        self._rec("free_blocks", (pool.block_base, pool.n_blocks), list(reqs))
+        self._w.free_blocks(pool, reqs)
+
+    def copy_prefix_row(self, src_row: int, dst_row: int, n_blocks: int) -> None:
+        self._rec("copy_prefix_row", src_row, dst_row, n_blocks)
+        self._w.copy_prefix_row(src_row, dst_row, n_blocks)
+
+    def copy_first_token(self, src_row: int, dst_row: int) -> None:
+        self._rec("copy_first_token", src_row, dst_row)
+        self._w.copy_first_token(src_row, dst_row)
+
+    def forward(self, plan) -> int:
+        self._rec("forward", plan)
+        self.flush()  # pickled before forward() reorders the plan
+        return self._w.forward(plan)
+
+    def forward_prefill_chunk(self, seq) -> int:
+        from .model import StepPlan
+
+        return self.forward(StepPlan(prefill=[seq]))
+
+    def forward_decode(self, toks) -> int:
+        from .model import StepPlan
+
+        return self.forward(StepPlan(decode=toks))
+
+    def collective(self, kind: str, *args) -> None:
+        """Tell the follower to join the next process-group collective (bench plumbing)."""
+        self._rec("collective", kind, args)
+        self.flush()
+
+    def stop(self) -> None:
+        self._rec("stop")
+        self.flush()
+
+
+class _Pool:
+    """The follower's copy of one engine's block pool (bitmap starts all free)."""
+
+    def __init__(self, worker, block_base: int, n_blocks: int) -> None:
+        import numpy as np
+
+        self.block_base, self.n_blocks = block_base, n_blocks
+        nwords = (n_blocks + 31) // 32
+        words = np.zeros(nwords, dtype=np.uint64)
+        full, rem = divmod(n_blocks, 32)
+        words[:full] = 0xFFFFFFFF
+        if rem:
+            words[full] = (1 << rem) - 1
+        self.bitmap = torch.from_numpy(words.astype(np.uint32).view(np.int32)).to(worker.device)
+
+
+class TpFollower:
+    """Replays the leader's device calls on this rank's shard until "stop"."""
+
+    def __init__(self, worker, ring: ByteRing, on_collective=None) -> None:
+        self.w, self.ring = worker, ring
+        self.pools: dict[int, _Pool] = {}
+        self.on_collective = on_collective  # fn(kind, args) joining the leader's collective
+        self.forwards = 0
+
+    def _pool(self, key) -> _Pool:
+        base, n = key
+        p = self.pools.get(base)
+        if p is None:
+            p = self.pools[base] = _Pool(self.w, base, n)
+        return p
+
+    def apply(self, ops_list) -> bool:
+        """Apply one message; False once the leader said stop."""
+        w = self.w
+        for op in ops_list:
+            name = op[0]
+            if name == "forward":
+                w.forward(op[1])
+                self.forwards += 1
+            elif name in ("alloc_blocks", "free_blocks"):
+                getattr(w, name)(self._pool(op[1]), op[2])
+            elif name in ("copy_prefix_row", "copy_first_token"):
+                getattr(w, name)(*op[1:])
+            elif name == "collective":
+                if self.on_collective is None:
+                    raise RuntimeError("leader issued a collective the follower cannot join")
+                self.on_collective(op[1], op[2])
+            elif name == "stop":
+                return False
+            else:
+                raise ValueError(f"unknown TP op {name!r}")
+        return True
+
+    def serve(self, idle_sleep: float = 0.0) -> None:
+        import time
+
+        while True:
+            msg = self.ring.recv()
+            if msg is None:
+                time.sleep(idle_sleep)
+                continue
+            if not self.apply(pickle.loads(msg)):
+                return
+
+
+def open_replica_ring(dist, replica: int, tp_rank: int, cap: int = 1 << 24) -> ByteRing:
+    """Create (leader) / attach (follower) the replica's call ring in /dev/shm.
+    Collective over the default process group (a name broadcast and two barriers)."""
+    obj = [f"{os.getpid()}_{os.environ.get('MASTER_PORT', '0')}"]
+    dist.broadcast_object_list(obj, src=0)
+    shm = "/dev/shm" if os.path.isdir("/dev/shm") else "/tmp"
+    path = os.path.join(shm, f"cortex_tp_{obj[0]}_{replica}")
+    ring = ByteRing(path, create=True, cap=cap) if tp_rank == 0 else None
+    dist.barrier()
+    if ring is None:
+        ring = ByteRing(path, create=False, cap=cap)
+    dist.barrier()
+    return ring

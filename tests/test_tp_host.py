@@ -77,3 +77,128 @@ def test_shards_sum_to_the_full_layer():
 
     torch.testing.assert_close(mlp(sc, parts[0]) + mlp(sc, parts[1]), mlp(cfg, w), rtol=1e-5,
                                atol=1e-5)
+
+
+# ------------------------------------------------------------------ replica host side
+
+
+def _logging_worker(n_eng, conc):
+    from harness import HostWorker
+    from paper_2510_14126_b200.engine import EngineParams, blocks_for
+
+    class LogWorker(HostWorker):
+        def forward(self, plan):
+            self.log.append(("forward", [(d.row, d.prefix_len, d.kv_len, d.hist_pos)
+                                         for d in plan.decode],
+                             [(s.row, s.prefix_len, s.kv_len, s.tokens.tolist(), s.out_row)
+                              for s in plan.prefill]))
+            return super().forward(plan)
+
+    params = EngineParams(1000 + conc * 450, 5000.0, 0.02, 0.1, conc)
+    return LogWorker(n_eng * blocks_for(params), n_eng * (conc + 4)), params
+
+
+def _run_leader(worker, params, conc=8, n_wf=40, mid=None):
+    from paper_2510_14126_b200.runtime import PoolRuntime
+    from paper_2510_14126_b200.workflow import Constant, Nl2Sql
+
+    spec = Nl2Sql(retry_budget=5, executor_service_time=Constant(0.0))
+    rt = PoolRuntime(worker, spec, params, concurrency=conc, n_workflows=n_wf, seed=0,
+                     prefill_budget=2048)
+    rt.fill()
+    rt.run_until(n_wf // 2)
+    if mid is not None:
+        mid()
+    rt.run_until(n_wf)
+    return sorted((wf.rid, wf.terminal, tuple(wf.history)) for wf in rt.finished)
+
+
+def test_tp_leader_follower_mirror_in_process(tmp_path):
+    """The follower replays exactly the leader's device calls; the proxy does not
+    change scheduling (outcomes equal a TP = 1 run)."""
+    from paper_2510_14126_b200.tp import ByteRing, TpFollower, TpLeader
+
+    plain, params = _logging_worker(2, 8)
+    out_plain = _run_leader(plain, params)
+    lw, _ = _logging_worker(2, 8)
+    fw, _ = _logging_worker(2, 8)
+    ring = ByteRing(str(tmp_path / "ring"), create=True, cap=1 << 22)
+    leader = TpLeader(lw, ring)
+    fol = TpFollower(fw, ByteRing(str(tmp_path / "ring"), create=False, cap=1 << 22))
+    drained = []
+
+    def drain():  # the follower keeps up (single process: drain between steps)
+        while (m := fol.ring.recv()) is not None:
+            import pickle
+
+            drained.append(fol.apply(pickle.loads(m)))
+
+    orig = lw.forward
+
+    def fwd(plan):
+        n = orig(plan)
+        drain()
+        return n
+
+    lw.forward = fwd
+    out_tp = _run_leader(leader, params)
+    leader.stop()
+    drain()
+    assert out_tp == out_plain
+    assert drained[-1] is False and all(drained[:-1])
+    assert len(lw.log) > 100
+    assert fw.log == lw.log == plain.log
+    assert fol.forwards == lw.steps
+    ring.close()
+
+
+def _two_rank(rank, port, path, out):
+    import os
+    import pickle
+
+    import torch.distributed as dist
+
+    from paper_2510_14126_b200.tp import ByteRing, TpFollower, TpLeader
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    w, params = _logging_worker(2, 8)
+    if rank == 0:
+        ring = ByteRing(path, create=True, cap=1 << 22)
+        dist.barrier()
+        leader = TpLeader(w, ring)
+
+        def mid():
+            leader.collective("barrier")
+            dist.barrier()
+
+        res = _run_leader(leader, params, mid=mid)
+        leader.stop()
+    else:
+        dist.barrier()
+        ring = ByteRing(path, create=False, cap=1 << 22)
+        TpFollower(w, ring, on_collective=lambda kind, args: dist.barrier()).serve()
+        res = None
+    dist.barrier()
+    with open(f"{out}.{rank}", "wb") as f:
+        pickle.dump((res, w.log), f)
+    ring.close()
+    dist.destroy_process_group()
+
+
+def test_tp_leader_follower_two_processes(tmp_path):
+    import pickle
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = str(tmp_path / "res")
+    mp.start_processes(_two_rank, args=(port, str(tmp_path / "ring2"), out), nprocs=2,
+                       join=True, start_method="spawn")
+    (res0, log0), (_, log1) = [pickle.load(open(f"{out}.{r}", "rb")) for r in (0, 1)]
+    plain, params = _logging_worker(2, 8)
+    assert res0 == _run_leader(plain, params)
+    assert log0 == log1 == plain.log
