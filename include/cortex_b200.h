@@ -109,6 +109,16 @@ int32_t cortex_gemm_set_mode(int32_t mode);
 int32_t cortex_gemm_set_stream_k(int32_t force);
 /* The 2-SM kernel's plan for (M, N, K): TN | (stream_k << 16). */
 int32_t cortex_gemm2_tile(int32_t M, int32_t N, int32_t K);
+/* Cluster split-K plan for decode-sized M: K splits (>= 1; 0 = not used), the token
+ * tile, token tiles and 256-row weight sub-tiles per CTA pair; cortex_gemm_splitk_force pins the split count (-1 = automatic; tuning/tests). */
+int32_t cortex_gemm_splitk_plan(int32_t M, int32_t N, int32_t K, int32_t* tn_out);
+int32_t cortex_gemm_splitk_plan2(int32_t M, int32_t N, int32_t K, int32_t* tn_out,
+                                 int32_t* m_tiles_out);
+int32_t cortex_gemm_splitk_plan3(int32_t M, int32_t N, int32_t K, int32_t* tn_out,
+                                 int32_t* m_tiles_out, int32_t* weight_subtiles_out);
+int32_t cortex_gemm_splitk_force(int32_t ks);
+int32_t cortex_gemm_splitk_force_mt(int32_t m_tiles);
+int32_t cortex_gemm_splitk_force_nw(int32_t weight_subtiles); /* 2: wide N unsplit; -1 auto */
 int32_t cortex_gemm_bf16(const void* tmap_w, const void* tmap_x, int32_t M, int32_t N, int32_t K,
                          void* out, int32_t ldo, int32_t out_f32, const void* residual,
                          int32_t ldr, float* workspace, uint64_t workspace_bytes,

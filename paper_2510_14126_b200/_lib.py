@@ -32,6 +32,12 @@ SIGNATURES: dict[str, list] = {
     "cortex_gemm_set_mode": [I32],
     "cortex_gemm_set_stream_k": [I32],
     "cortex_gemm2_tile": [I32, I32, I32],
+    "cortex_gemm_splitk_plan": [I32, I32, I32, P],
+    "cortex_gemm_splitk_plan2": [I32, I32, I32, P, P],
+    "cortex_gemm_splitk_plan3": [I32, I32, I32, P, P, P],
+    "cortex_gemm_splitk_force": [I32],
+    "cortex_gemm_splitk_force_mt": [I32],
+    "cortex_gemm_splitk_force_nw": [I32],
     "cortex_gemm_bf16": [P, P, I32, I32, I32, P, I32, I32, P, I32, P, U64, P, I32, P],
     "cortex_embed": [P, P, P, I32, I32, P, P],
     "cortex_rmsnorm": [P, P, I32, P, I32, F32, P, P],

@@ -309,25 +309,37 @@ int32_t cortex_gemm_2sm_launch(const void* tmap_w, const void* tmap_x, int32_t M
                                uint64_t workspace_bytes, int32_t* counters, int32_t n_counters,
                                cudaStream_t stream);
 
+extern "C" int32_t cortex_gemm_splitk_plan(int32_t M, int32_t N, int32_t K, int32_t* tn_out);
+extern "C" int32_t cortex_gemm_splitk_launch(const void* tmap_w, const void* tmap_x, int32_t M,
+                                             int32_t N, int32_t K, void* out, int32_t ldo,
+                                             int32_t out_f32, const void* residual, int32_t ldr,
+                                             float* workspace, uint64_t workspace_bytes,
+                                             cudaStream_t stream);
+
 namespace {
-int g_gemm_mode = 0;  // 0 auto, 1 force the 1-SM (split-K) kernel, 2 force 2-SM when legal
+// 0 auto, 1 force the 1-SM (split-K) kernel, 2 force 2-SM when legal, 3 force the
+// cluster split-K 2-SM kernel when it has a plan
+int g_gemm_mode = 0;
 }
 
 extern "C" {
 
 // Kernel choice: 1 = 1-SM swap-AB kernel with split-K (decode-sized, weight-streaming
-// bound), 2 = persistent 2-SM kernel (M > 128, compute bound; needs N % 256 == 0).
+// bound; N % 256 != 0 or too many tiles for a split plan), 2 = persistent 2-SM kernel
+// (M > 128, compute bound; needs N % 256 == 0).
+// 3 = cluster split-K 2-SM kernel (gemm_splitk.cu: decode-sized M with few 256-row tiles).
 int32_t cortex_gemm_path(int32_t M, int32_t N, int32_t K) {
-  (void)K;
   const bool legal2 = (N % 256) == 0;
   if (g_gemm_mode == 1 || !legal2) return 1;
   if (g_gemm_mode == 2) return 2;
+  if (cortex_gemm_splitk_plan(M, N, K, nullptr) >= 1) return 3;
+  if (g_gemm_mode == 3) return 2;
   return M > 128 ? 2 : 1;
 }
 
-// Test hook: 0 auto, 1 force 1-SM, 2 force 2-SM.
+// Test hook: 0 auto, 1 force 1-SM, 2 force 2-SM, 3 prefer the cluster split-K kernel.
 int32_t cortex_gemm_set_mode(int32_t mode) {
-  if (mode < 0 || mode > 2) return CORTEX_EBADARG;
+  if (mode < 0 || mode > 3) return CORTEX_EBADARG;
   g_gemm_mode = mode;
   return CORTEX_OK;
 }
@@ -403,7 +415,11 @@ int32_t cortex_gemm_bf16(const void* tmap_w, const void* tmap_x, int32_t M, int3
                          int32_t* counters, int32_t n_counters, cudaStream_t stream) {
   if (!tmap_w || !tmap_x || !out || M <= 0 || N <= 0 || K <= 0 || N % kBlockN || K % kBlockK)
     return CORTEX_EBADARG;
-  if (cortex_gemm_path(M, N, K) == 2)
+  const int path = cortex_gemm_path(M, N, K);
+  if (path == 3)
+    return cortex_gemm_splitk_launch(tmap_w, tmap_x, M, N, K, out, ldo, out_f32, residual, ldr,
+                                     workspace, workspace_bytes, stream);
+  if (path == 2)
     return cortex_gemm_2sm_launch(tmap_w, tmap_x, M, N, K, out, ldo, out_f32, residual, ldr,
                                   workspace, workspace_bytes, counters, n_counters, stream);
   GemmArgs a{};

@@ -10,10 +10,12 @@ Run with `pytest -m gpu`. Tolerances (north star: "2e-3 relative error in bf16")
 
 from __future__ import annotations
 
+import ctypes
 import math
 import random
 
 import numpy as np
+
 import pytest
 import torch
 
@@ -134,22 +136,111 @@ def test_gemm_fused_swiglu(cuda, mode, M, F, K):
     assert rel(out, ref) < 4e-3
 
 
+@pytest.mark.parametrize("ks", [-1, 2, 3, 4])
+@pytest.mark.parametrize("M,N,K", [(129, 4096, 4096), (210, 6144, 4096), (256, 4096, 14336),
+                                   (200, 512, 256), (5, 4096, 4096), (64, 1024, 768),
+                                   (100, 28672, 4096)])
+def test_gemm_splitk_cluster(cuda, ks, M, N, K):
+    """Cluster split-K 2-SM kernel (gemm_splitk.cu) with every split count: bf16 out,
+    fp32 out with the residual added in place, and the fused SwiGLU epilogue."""
+    o = ops()
+    L = o.lib()
+    g = torch.Generator(device=cuda).manual_seed(M * 7 + N + K)
+    x = torch.randn(max(M, 32), K, generator=g, device=cuda).to(torch.bfloat16)
+    w = (torch.randn(N, K, generator=g, device=cuda) * 0.05).to(torch.bfloat16)
+    r = torch.randn(M, N, generator=g, device=cuda)
+    ws = o.GemmWorkspace(cuda)
+    o.gemm_set_mode(3)
+    assert L.cortex_gemm_splitk_force(ks) == 0
+    try:
+        kb = K // 64
+        got = L.cortex_gemm_splitk_plan(M, N, K, None)
+        if ks > 0 and got:  # the forced count, or no plan (it would not fit one wave)
+            assert got == ks and (got - 1) * -(-kb // got) < kb
+        assert got != 1  # (no split only when forced: see test_gemm_splitk_nw2)
+        path = o.gemm_path(M, N, K)
+        out = torch.full((M, N), float("nan"), device=cuda, dtype=torch.bfloat16)
+        o.gemm(o.weight_map(w), o.act_map(x), M, out, ws)
+        res = r.clone()
+        o.gemm(o.weight_map(w), o.act_map(x), M, res, ws, residual=res)
+        wi = o.interleave_gate_up(w)
+        act = torch.full((M, N // 2), float("nan"), device=cuda, dtype=torch.bfloat16)
+        o.gemm(o.weight_map(wi), o.act_map(x), M, act, ws, swiglu=True)
+        torch.cuda.synchronize()
+    finally:
+        o.gemm_set_mode(0)
+        L.cortex_gemm_splitk_force(-1)
+    assert path == (3 if got >= 1 else 2)
+    ref = x[:M].float() @ w.float().T
+    assert torch.isfinite(out.float()).all()
+    assert rel(out, ref) < 4e-3
+    assert rel(res, ref + r) < 4e-5
+    gg, uu = ref[:, :N // 2], ref[:, N // 2:]
+    assert rel(act, gg / (1 + torch.exp(-gg)) * uu) < 4e-3
+
+
+@pytest.mark.parametrize("M,N,K", [(100, 28672, 4096), (233, 28672, 4096), (17, 20480, 512)])
+def test_gemm_splitk_nw2(cuda, M, N, K):
+    """The kernel's unsplit mode with two 256-row weight sub-tiles per pair (forced; the
+    automatic plan keeps wide projections on the persistent 2-SM kernel)."""
+    o = ops()
+    L = o.lib()
+    g = torch.Generator(device=cuda).manual_seed(M + N)
+    x = torch.randn(max(M, 32), K, generator=g, device=cuda).to(torch.bfloat16)
+    w = (torch.randn(N, K, generator=g, device=cuda) * 0.05).to(torch.bfloat16)
+    ws = o.GemmWorkspace(cuda)
+    assert L.cortex_gemm_splitk_force_nw(2) == 0
+    try:
+        nw = ctypes.c_int32()
+        assert L.cortex_gemm_splitk_plan3(M, N, K, None, None, ctypes.byref(nw)) == 1
+        assert nw.value == 2 and o.gemm_path(M, N, K) == 3
+        out = torch.full((M, N), float("nan"), device=cuda, dtype=torch.bfloat16)
+        o.gemm(o.weight_map(w), o.act_map(x), M, out, ws)
+        act = torch.full((M, N // 2), float("nan"), device=cuda, dtype=torch.bfloat16)
+        o.gemm(o.weight_map(o.interleave_gate_up(w)), o.act_map(x), M, act, ws, swiglu=True)
+        torch.cuda.synchronize()
+    finally:
+        L.cortex_gemm_splitk_force_nw(-1)
+    ref = x[:M].float() @ w.float().T
+    assert rel(out, ref) < 4e-3
+    gg, uu = ref[:, :N // 2], ref[:, N // 2:]
+    assert rel(act, gg / (1 + torch.exp(-gg)) * uu) < 4e-3
+
+
+def test_gemm_splitk_deterministic(cuda):
+    """The split reduction runs in split order: repeated launches agree bit for bit."""
+    o = ops()
+    M, N, K = 210, 4096, 14336
+    g = torch.Generator(device=cuda).manual_seed(11)
+    x = torch.randn(M, K, generator=g, device=cuda).to(torch.bfloat16)
+    w = (torch.randn(N, K, generator=g, device=cuda) * 0.05).to(torch.bfloat16)
+    ws = o.GemmWorkspace(cuda)
+    assert o.gemm_path(M, N, K) == 3
+    outs = []
+    for _ in range(3):
+        out = torch.empty(M, N, device=cuda)
+        o.gemm(o.weight_map(w), o.act_map(x), M, out, ws)
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+
+
 def test_gemm_batch_invariant(cuda):
-    """Within the decode regime (M <= 128, the 1-SM kernel, split-K fixed by N and K) a
-    row's result does not depend on the other rows of the batch."""
+    """Within the decode regime (M <= 256: the cluster split-K kernel, whose split count is
+    fixed by N and K) a row's result does not depend on the other rows of the batch."""
     o = ops()
     N, K = 6144, 4096
     g = torch.Generator(device=cuda).manual_seed(3)
-    x = torch.randn(128, K, generator=g, device=cuda).to(torch.bfloat16)
+    x = torch.randn(256, K, generator=g, device=cuda).to(torch.bfloat16)
     w = (torch.randn(N, K, generator=g, device=cuda) * 0.05).to(torch.bfloat16)
     ws = o.GemmWorkspace(cuda)
-    full = torch.empty(128, N, device=cuda, dtype=torch.bfloat16)
-    assert o.gemm_path(128, N, K) == 1
-    o.gemm(o.weight_map(w), o.act_map(x), 128, full, ws)
-    for m in (1, 17, 64, 100):
+    full = torch.empty(256, N, device=cuda, dtype=torch.bfloat16)
+    assert o.gemm_path(256, N, K) == 3
+    o.gemm(o.weight_map(w), o.act_map(x), 256, full, ws)
+    for m in (1, 17, 64, 100, 129, 200):
+        assert o.gemm_path(m, N, K) == 3
         part = torch.empty(m, N, device=cuda, dtype=torch.bfloat16)
         o.gemm(o.weight_map(w), o.act_map(x), m, part, ws)
-        assert torch.equal(part, full[:m])
+        assert torch.equal(part, full[:m]), m
 
 
 # ---------------------------------------------------------------- attention
