@@ -36,7 +36,8 @@ def test_library_loads_and_exports_everything():
     # balanced plan: 2 waves of 55 chunks x 8 kv heads on 148 SMs -> 37 tiles per chunk
     assert lib.cortex_decode_tiles_per_chunk(4000, 8) == 37
     assert lib.cortex_gemm_path(700, 4096, 4096) == 2
-    assert lib.cortex_gemm_path(64, 4096, 4096) == 1
+    assert lib.cortex_gemm_path(64, 4096, 4096) == 3  # cluster split-K (decode M)
+    assert lib.cortex_gemm_path(64, 128256, 4096) == 1  # lm_head: too many tiles to split
 
 
 def test_no_cpu_fallback_without_library(monkeypatch, tmp_path):
