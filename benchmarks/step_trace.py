@@ -78,6 +78,24 @@ def main() -> None:
         ivs.append((t0, t1))
         per[cls][0] += 1
         per[cls][1] += (t1 - t0) / 1e3
+    # gaps on the GPU timeline (all streams merged): idle time before each kernel class
+    evs = sorted((ev.time_range.start, ev.time_range.end,
+                  ev.name.replace("void ", "").replace("(anonymous namespace)::", "").split("(")[0]
+                  .split("<")[0])
+                 for ev in prof.events() if ev.device_type == torch.autograd.DeviceType.CUDA)
+    gaps = defaultdict(lambda: [0, 0.0])
+    end = evs[0][1]
+    prev = evs[0][2]
+    for a, b, nm in evs[1:]:
+        if a > end:
+            key = f"{prev} -> {nm}"
+            gaps[key][0] += 1
+            gaps[key][1] += (a - end) / 1e3
+        if b > end:
+            end, prev = b, nm
+    print("largest idle gap classes (count, total ms):")
+    for k, (n, ms) in sorted(gaps.items(), key=lambda kv: -kv[1][1])[:14]:
+        print(f"  {k[:90]:90s} {n:6d} {ms:8.3f} ms  avg {1e3 * ms / n:6.2f} us")
     ivs.sort()
     busy = 0.0
     cur0, cur1 = ivs[0]

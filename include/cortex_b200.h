@@ -48,6 +48,11 @@ enum {
 /* ABI version (major * 100 + minor). */
 int32_t cortex_abi_version(void);
 
+/* Programmatic dependent launch for the decoder-step kernels (1 = on, the default; 0 =
+ * off): each kernel is launched while its predecessor on the stream runs and waits for it
+ * in-kernel after its prologue. */
+int32_t cortex_set_pdl(int32_t on);
+
 /* ---- KV block pool (bitmap, bit = 1 -> free) -------------------------------
  * EngineState.admit (engines.py:142-166): cold prefix blocks + prompt blocks;
  * the lazy per-16-token append during EngineState.advance_decode

@@ -22,6 +22,7 @@ F32 = c_float
 # name -> argtypes (every export returns int32 status)
 SIGNATURES: dict[str, list] = {
     "cortex_abi_version": [],
+    "cortex_set_pdl": [I32],
     "cortex_kv_alloc": [P, I32, I32, P, P, P, I32, P, I32, P, P],
     "cortex_kv_free": [P, I32, I32, P, I32, P, P, P, I32, P, P],
     "cortex_table_copy": [P, I32, P, P, P, P, I32, P],
@@ -92,6 +93,8 @@ def load() -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.argtypes = argtypes
             fn.restype = c_int32
+        if os.environ.get("CORTEX_PDL") == "0":  # A/B runs without programmatic launch
+            lib.cortex_set_pdl(0)
         _LIB = lib
     return _LIB
 

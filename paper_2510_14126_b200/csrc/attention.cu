@@ -457,6 +457,8 @@ CORTEX_DEVICE int tile_nvalid(int prefix, int kvlen, int j) {
 
 __global__ void __launch_bounds__(kWarps * 32)
     paged_decode_kernel(const __grid_constant__ CUtensorMap tmap_kv, const DecodeArgs a) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -569,6 +571,8 @@ inline size_t flat_smem_bytes(int group) {
 
 __global__ void __launch_bounds__(kWarps * 32)
     paged_decode_flat_kernel(const __grid_constant__ CUtensorMap tmap_kv, const FlatArgs f) {
+  pdl_wait();
+  pdl_trigger();
   const DecodeArgs& a = f.d;
   // Shared memory: a 2 KiB static block (metadata, barriers, merge scalars), then the
   // dynamic stages + merge area starting 1 KiB-aligned (the SW128 TMA boxes need it).
@@ -729,6 +733,8 @@ struct CascadeArgs {
 
 __global__ void __launch_bounds__(kWarps * 32)
     cascade_prefix_kernel(const __grid_constant__ CUtensorMap tmap_kv, const CascadeArgs a) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -840,6 +846,8 @@ struct CombineArgs {
 constexpr int kCombineThreads = 256;
 
 __global__ void __launch_bounds__(kCombineThreads) decode_combine_kernel(const CombineArgs a) {
+  pdl_wait();
+  pdl_trigger();
   const int b = blockIdx.x;
   const int warp = warp_id();
   const int lane = lane_id();
@@ -967,6 +975,8 @@ struct PrefillArgs {
 
 __global__ void __launch_bounds__(kWarps * 32)
     paged_prefill_kernel(const __grid_constant__ CUtensorMap tmap_kv, const PrefillArgs a) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -1150,9 +1160,9 @@ int32_t cortex_paged_decode_attn_flat(
     }
     const int spc = (16 / group) * kWarps;
     dim3 cgrid((max_group_count + spc - 1) / spc, n_kv_heads, n_groups * prefix_slots);
-    cascade_prefix_kernel<<<cgrid, kWarps * 32, csmem, stream>>>(
-        *reinterpret_cast<const CUtensorMap*>(tmap_kv), c);
-    CORTEX_CHECK_LAUNCH();
+    if (pdl_launch(cascade_prefix_kernel, cgrid, kWarps * 32, csmem, stream, 1,
+                   *reinterpret_cast<const CUtensorMap*>(tmap_kv), c) != cudaSuccess)
+      return CORTEX_ECUDA;
   }
   DecodeArgs a{};
   a.q = reinterpret_cast<const __nv_bfloat16*>(q);
@@ -1196,14 +1206,14 @@ int32_t cortex_paged_decode_attn_flat(
       fconf = static_cast<int>(fsmem);
     }
     dim3 grid((total_tiles + tiles_per_chunk - 1) / tiles_per_chunk, n_kv_heads);
-    paged_decode_flat_kernel<<<grid, kWarps * 32, fsmem, stream>>>(
-        *reinterpret_cast<const CUtensorMap*>(tmap_kv), fa);
-    CORTEX_CHECK_LAUNCH();
+    if (pdl_launch(paged_decode_flat_kernel, grid, kWarps * 32, fsmem, stream, 1,
+                   *reinterpret_cast<const CUtensorMap*>(tmap_kv), fa) != cudaSuccess)
+      return CORTEX_ECUDA;
   } else if ((parts & 2) && !seq_tile_start) {
     dim3 grid(max_splits - a.slot_off, n_kv_heads, n_seqs);
-    paged_decode_kernel<<<grid, kWarps * 32, smem, stream>>>(
-        *reinterpret_cast<const CUtensorMap*>(tmap_kv), a);
-    CORTEX_CHECK_LAUNCH();
+    if (pdl_launch(paged_decode_kernel, grid, kWarps * 32, smem, stream, 1,
+                   *reinterpret_cast<const CUtensorMap*>(tmap_kv), a) != cudaSuccess)
+      return CORTEX_ECUDA;
   }
   if (!(parts & 4)) return CORTEX_OK;
   CombineArgs cb{};
@@ -1219,8 +1229,8 @@ int32_t cortex_paged_decode_attn_flat(
   cb.tile_start = seq_tile_start;
   cb.W = tiles_per_chunk;
   const dim3 cgrid(n_seqs, (cb.hq + kCombineThreads / 32 - 1) / (kCombineThreads / 32));
-  decode_combine_kernel<<<cgrid, kCombineThreads, 0, stream>>>(cb);
-  CORTEX_CHECK_LAUNCH();
+  if (pdl_launch(decode_combine_kernel, cgrid, kCombineThreads, 0, stream, 1, cb) != cudaSuccess)
+    return CORTEX_ECUDA;
   return CORTEX_OK;
 }
 
@@ -1298,9 +1308,9 @@ int32_t cortex_paged_prefill_attn(const void* tmap_kv, const void* q, void* out,
   }
   const int toks_per_cta = (16 / group) * kWarps;
   dim3 grid((max_qlen + toks_per_cta - 1) / toks_per_cta, n_kv_heads, n_seqs);
-  paged_prefill_kernel<<<grid, kWarps * 32, smem, stream>>>(
-      *reinterpret_cast<const CUtensorMap*>(tmap_kv), a);
-  CORTEX_CHECK_LAUNCH();
+  if (pdl_launch(paged_prefill_kernel, grid, kWarps * 32, smem, stream, 1,
+                 *reinterpret_cast<const CUtensorMap*>(tmap_kv), a) != cudaSuccess)
+    return CORTEX_ECUDA;
   return CORTEX_OK;
 }
 

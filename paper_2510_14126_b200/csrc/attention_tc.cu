@@ -218,6 +218,8 @@ CORTEX_DEVICE float ex2_approx(float x) {  // 2^x, one MUFU op (-inf -> 0)
 __global__ void __launch_bounds__(kThreadsTC, 1)
     fmha_tc_kernel(const __grid_constant__ CUtensorMap tmap_q,
                    const __grid_constant__ CUtensorMap tmap_kv, const FmhaArgs a) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -572,8 +574,8 @@ int32_t launch_fmha(const CUtensorMap* tq, const CUtensorMap* tkv, const FmhaArg
       return CORTEX_ECUDA;
     configured = true;
   }
-  fmha_tc_kernel<<<grid, kThreadsTC, kSmemTC, stream>>>(*tq, *tkv, a);
-  CORTEX_CHECK_LAUNCH();
+  if (pdl_launch(fmha_tc_kernel, grid, kThreadsTC, kSmemTC, stream, 1, *tq, *tkv, a) != cudaSuccess)
+    return CORTEX_ECUDA;
   return CORTEX_OK;
 }
 

@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #ifndef __CUDACC__
 #error "common.cuh is CUDA-only"
 #endif
@@ -24,6 +26,45 @@
     cudaError_t _e = cudaGetLastError();           \
     if (_e != cudaSuccess) return CORTEX_ECUDA;    \
   } while (0)
+
+// --------------------------------------------------------------------------
+// Programmatic dependent launch (PDL). The decoder step is a chain of ~10 kernels per
+// layer on one stream; with PDL a kernel is launched while its predecessor still runs,
+// does its prologue (barrier init, TMEM allocation, descriptor prefetch), and blocks in
+// pdl_wait() until the predecessor has completed and its memory is visible. Every kernel
+// launched through pdl_launch() must call pdl_wait() before it touches memory an earlier
+// kernel of the stream writes. pdl_trigger() lets the next kernel launch once every CTA
+// of this grid has triggered (or exited). g_cortex_pdl = 0 turns the attribute off.
+
+extern int g_cortex_pdl;
+
+CORTEX_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+CORTEX_DEVICE void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" :::); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, int cluster_x, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[n].val.programmaticStreamSerializationAllowed = g_cortex_pdl ? 1 : 0;
+  ++n;
+  if (cluster_x > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = cluster_x;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // --------------------------------------------------------------------------
 // generic

@@ -32,6 +32,8 @@ CORTEX_DEVICE bf16x8 pack8(const float (&f)[8]) {
 // out[t] = float(emb[tok]), tok = tokens[index ? index[t] : t]  (fp32 residual stream)
 __global__ void embed_kernel(const __nv_bfloat16* __restrict__ emb, const int* __restrict__ tokens,
                              const int* __restrict__ index, int d, float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int t = blockIdx.x;
   const int tok = tokens[index ? index[t] : t];
   const bf16x8* src = reinterpret_cast<const bf16x8*>(emb + static_cast<int64_t>(tok) * d);
@@ -60,6 +62,8 @@ CORTEX_DEVICE float block_sum(float v, float* red) {
 __global__ void rmsnorm_kernel(const float* __restrict__ x, const int* __restrict__ rows,
                                const __nv_bfloat16* __restrict__ w, int d, float eps,
                                __nv_bfloat16* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[32];
   const int r = blockIdx.x;
   const int src = rows ? rows[r] : r;
@@ -115,6 +119,8 @@ struct RopeArgs {
 };
 
 __global__ void rope_kv_append_kernel(const RopeArgs a) {
+  pdl_wait();
+  pdl_trigger();
   const int t = blockIdx.x;
   const int pos = a.tok_pos[t];
   const int ldq = (a.hq + 2 * a.hkv) * kHeadDim;
@@ -184,6 +190,8 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int64_t ld, int 
                               int* __restrict__ out_tok, const int* __restrict__ slot,
                               int* __restrict__ slot_tok, int* __restrict__ hist,
                               int hist_stride, const int* __restrict__ hist_pos) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float sv[32];
   __shared__ int si[32];
   const int r = blockIdx.x;
@@ -235,9 +243,10 @@ int32_t cortex_embed(const void* emb, const int32_t* tokens, const int32_t* inde
                      int32_t d, void* out, cudaStream_t stream) {
   if (!emb || !tokens || !out || n_tok < 0 || d % 8) return CORTEX_EBADARG;
   if (n_tok == 0) return CORTEX_OK;
-  embed_kernel<<<n_tok, 128, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(emb), tokens,
-                                          index, d, reinterpret_cast<float*>(out));
-  CORTEX_CHECK_LAUNCH();
+  if (pdl_launch(embed_kernel, n_tok, 128, 0, stream, 1,
+                 reinterpret_cast<const __nv_bfloat16*>(emb), tokens, index, d,
+                 reinterpret_cast<float*>(out)) != cudaSuccess)
+    return CORTEX_ECUDA;
   return CORTEX_OK;
 }
 
@@ -248,10 +257,11 @@ int32_t cortex_rmsnorm(const void* x, const int32_t* rows, int32_t n_rows, const
   int threads = 32;
   while (threads * 8 * 4 < d) threads *= 2;
   if (threads < 64) threads = 64;
-  rmsnorm_kernel<<<n_rows, threads, 0, stream>>>(
-      reinterpret_cast<const float*>(x), rows, reinterpret_cast<const __nv_bfloat16*>(w),
-      d, eps, reinterpret_cast<__nv_bfloat16*>(y));
-  CORTEX_CHECK_LAUNCH();
+  if (pdl_launch(rmsnorm_kernel, n_rows, threads, 0, stream, 1,
+                 reinterpret_cast<const float*>(x), rows,
+                 reinterpret_cast<const __nv_bfloat16*>(w), d, eps,
+                 reinterpret_cast<__nv_bfloat16*>(y)) != cudaSuccess)
+    return CORTEX_ECUDA;
   return CORTEX_OK;
 }
 
@@ -281,8 +291,8 @@ int32_t cortex_rope_kv_append(const void* qkv, void* q_out, void* cache, int64_t
   a.sin_tab = sin_tab;
   a.hq = hq;
   a.hkv = hkv;
-  rope_kv_append_kernel<<<n_tok, 256, 0, stream>>>(a);
-  CORTEX_CHECK_LAUNCH();
+  if (pdl_launch(rope_kv_append_kernel, n_tok, 256, 0, stream, 1, a) != cudaSuccess)
+    return CORTEX_ECUDA;
   return CORTEX_OK;
 }
 
@@ -304,9 +314,9 @@ int32_t cortex_argmax(const float* logits, int64_t ld, int32_t n_rows, int32_t v
   if (!logits || n_rows < 0 || vocab <= 0) return CORTEX_EBADARG;
   if (hist && (!slot || !hist_pos)) return CORTEX_EBADARG;
   if (n_rows == 0) return CORTEX_OK;
-  argmax_kernel<<<n_rows, 1024, 0, stream>>>(logits, ld, vocab, out_tok, slot, slot_tok, hist,
-                                             hist_stride, hist_pos);
-  CORTEX_CHECK_LAUNCH();
+  if (pdl_launch(argmax_kernel, n_rows, 1024, 0, stream, 1, logits, ld, vocab, out_tok, slot,
+                 slot_tok, hist, hist_stride, hist_pos) != cudaSuccess)
+    return CORTEX_ECUDA;
   return CORTEX_OK;
 }
 

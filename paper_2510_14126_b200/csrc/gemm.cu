@@ -141,6 +141,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  pdl_wait();  // the activations (and residual) come from the previous kernel
+  pdl_trigger();
 
   if (warp == 0) {
     if (elect_one()) {
@@ -282,8 +284,8 @@ int32_t launch_gemm(const CUtensorMap* tw, const CUtensorMap* tx, const GemmArgs
       return CORTEX_ECUDA;
     configured = true;
   }
-  kern<<<grid, kThreads, L::kTotal, stream>>>(*tw, *tx, a);
-  CORTEX_CHECK_LAUNCH();
+  if (pdl_launch(kern, grid, kThreads, L::kTotal, stream, 1, *tw, *tx, a) != cudaSuccess)
+    return CORTEX_ECUDA;
   return CORTEX_OK;
 }
 

@@ -219,6 +219,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  pdl_wait();  // the activations (and residual) come from the previous kernel
+  pdl_trigger();
 
   if (warp == 0) {
     if (elect_one()) {
@@ -459,8 +461,9 @@ int32_t launch2(const CUtensorMap* tw, const CUtensorMap* tx, const Gemm2Args& a
   if (b.npairs > CORTEX_GEMM_MAXPAIRS) b.npairs = CORTEX_GEMM_MAXPAIRS;
 #endif
   if (b.sk && b.total_units < b.npairs) b.npairs = b.total_units;
-  kern<<<2 * b.npairs, kThreads2, L::kTotal, stream>>>(*tw, *tx, b);
-  CORTEX_CHECK_LAUNCH();
+  if (pdl_launch(kern, 2 * b.npairs, kThreads2, L::kTotal, stream, 1, *tw, *tx, b) !=
+      cudaSuccess)
+    return CORTEX_ECUDA;
   return CORTEX_OK;
 }
 

@@ -198,6 +198,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   SK_TRACE(1);
+  pdl_wait();  // the activations (and residual) come from the previous kernel
+  pdl_trigger();
   const uint16_t pair_mask = static_cast<uint16_t>(3u << lead);
 
   if (warp == 0) {
@@ -332,20 +334,9 @@ int32_t launch_sk(const CUtensorMap* tw, const CUtensorMap* tx, const SkArgs& a,
       return CORTEX_ECUDA;
     configured = true;
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(n_clusters * 2 * a.ks, 1, 1);
-  cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = L::kTotal;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2 * a.ks;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, kern, *tw, *tx, a) != cudaSuccess) return CORTEX_ECUDA;
-  CORTEX_CHECK_LAUNCH();
+  if (pdl_launch(kern, n_clusters * 2 * a.ks, kThreads, L::kTotal, stream, 2 * a.ks, *tw, *tx, a) !=
+      cudaSuccess)
+    return CORTEX_ECUDA;
   return CORTEX_OK;
 }
 

@@ -158,9 +158,18 @@ __global__ void popcount_kernel(const uint32_t* bitmap, int nwords, int* out_fre
 
 }  // namespace
 
+int g_cortex_pdl = 1;
+
 extern "C" {
 
 int32_t cortex_abi_version(void) { return 100; }
+
+// Programmatic dependent launch of the decoder-step kernels: 1 on (default), 0 off.
+int32_t cortex_set_pdl(int32_t on) {
+  if (on != 0 && on != 1) return CORTEX_EBADARG;
+  g_cortex_pdl = on;
+  return CORTEX_OK;
+}
 
 int32_t cortex_kv_alloc(uint32_t* bitmap, int32_t nblocks, int32_t id_base,
                         const int32_t* counts, const int32_t* rows, const int32_t* cols,

@@ -57,6 +57,8 @@ __global__ void tp_allreduce_rmsnorm_kernel(const float* y0, const float* y1,
                                             uint32_t epoch, int32_t* status) {
   __shared__ float red[32];
   __shared__ int timed_out;
+  pdl_wait();
+  pdl_trigger();
   if (threadIdx.x == 0) {
     timed_out = 0;
     if (flag) {
@@ -167,6 +169,7 @@ int32_t cortex_ipc_close(void* ptr) {
 
 int32_t cortex_tp_signal(uint32_t* peer_flag, uint32_t epoch, cudaStream_t stream) {
   if (!peer_flag) return CORTEX_EBADARG;
+  // a plain (non-PDL) launch: the signal must follow the partial GEMM's completion
   tp_signal_kernel<<<1, 1, 0, stream>>>(peer_flag, epoch);
   CORTEX_CHECK_LAUNCH();
   return CORTEX_OK;
@@ -181,10 +184,10 @@ int32_t cortex_tp_allreduce_rmsnorm(const float* y0, const float* y1, float* x, 
   if (n_rows == 0) return CORTEX_OK;
   int threads = 64;
   while (threads * 4 * 8 < d) threads *= 2;
-  tp_allreduce_rmsnorm_kernel<<<n_rows, threads, 0, stream>>>(
-      y0, y1, x, reinterpret_cast<const __nv_bfloat16*>(w), d, eps,
-      reinterpret_cast<__nv_bfloat16*>(out), flag, epoch, status);
-  CORTEX_CHECK_LAUNCH();
+  if (pdl_launch(tp_allreduce_rmsnorm_kernel, n_rows, threads, 0, stream, 1, y0, y1, x,
+                 reinterpret_cast<const __nv_bfloat16*>(w), d, eps,
+                 reinterpret_cast<__nv_bfloat16*>(out), flag, epoch, status) != cudaSuccess)
+    return CORTEX_ECUDA;
   return CORTEX_OK;
 }
 
