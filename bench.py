@@ -376,8 +376,18 @@ def main() -> None:
         bound, unit, peak = "hbm", "GB/s", peaks["hbm_gbs"]
         per_launch = kshare["bytes"] / max(kshare["launches"], 1)
         achieved = kshare["bytes"] / max(kshare["ms"] / 1e3, 1e-12) / 1e9
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):  # DRAM bytes per launch of this class from the committed ncu list
+        with open(tpath) as f:
+            tj = json.load(f)
+        if dominant in tj.get("classes", {}):
+            traffic = tj["classes"][dominant]["dram_bytes_per_launch"]
+            traffic_src = tj.get("source")
     roofline = {"kernel": dominant, "bound": bound, "achieved": achieved, "peak": peak,
-                "unit": unit, "frac": achieved / peak, "traffic": None,
+                "unit": unit, "frac": achieved / peak, "traffic": traffic,
+                "traffic_source": traffic_src,
+                "algorithmic_bytes_per_launch": kshare["bytes"] / max(kshare["launches"], 1),
                 "per_launch_algorithmic": per_launch, "avg_launch_ms": kshare["ms"] / max(
                     kshare["launches"], 1), "launches": kshare["launches"],
                 "peak_source": peak_src + (" sustained" if bound == "tensor" else "")}

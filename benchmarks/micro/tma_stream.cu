@@ -113,6 +113,47 @@ __global__ void mixed(const uint8_t* src, size_t slice, int chunk, int stages, f
   if (acc == 12345.f) sink[0] = acc;
 }
 
+
+// `nstreams` warps each run an independent bulk-TMA stream (own barriers and buffers) over
+// their own part of the CTA's slice: does the per-SM rate grow with issuing threads?
+__global__ void multi(const uint8_t* src, size_t slice, int chunk, int stages, int nstreams,
+                      float* sink) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ __align__(8) uint64_t bar[64];
+  const int w = threadIdx.x / 32;
+  if (w >= nstreams || (threadIdx.x & 31) != 0) return;
+  const size_t part = slice / nstreams / chunk * chunk;
+  const uint8_t* base = src + blockIdx.x * slice + w * part;
+  uint64_t* mb = bar + w * stages;
+  uint8_t* buf = sm + w * stages * chunk;
+  for (int s = 0; s < stages; ++s)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mb[s])));
+  asm volatile("fence.mbarrier_init.release.cluster;");
+  const int n = static_cast<int>(part / chunk);
+  float acc = 0.f;
+  for (int i = 0; i < n + stages; ++i) {
+    if (i >= stages) {
+      const int s = (i - stages) % stages;
+      const uint32_t ph = ((i - stages) / stages) & 1;
+      asm volatile(
+          "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+          " @!p bra W;\n}" ::"r"(su32(&mb[s])), "r"(ph));
+      acc += static_cast<float>(buf[s * chunk]);
+    }
+    if (i < n) {
+      const int s = i % stages;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&mb[s])),
+                   "r"(chunk));
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+          ::"r"(su32(buf + s * chunk)), "l"(base + static_cast<size_t>(i) * chunk), "r"(chunk),
+          "r"(su32(&mb[s]))
+          : "memory");
+    }
+  }
+  if (acc == 12345.f) sink[0] = acc;
+}
+
 int main() {
   const size_t total = size_t(1) << 30;  // 1 GiB read per launch (>> L2)
   uint8_t* src;
@@ -179,6 +220,28 @@ int main() {
     const double gbs = double(slice) * g * 5 / (ms * 1e-3) / 1e9;
     printf("%s{\"ctas\": %d, \"GBps\": %.0f, \"per_sm_GBps\": %.1f}", first ? "" : ",\n", g, gbs, gbs / g);
     first = false;
+  }
+  printf("\n], \"multi\": [\n");
+  first = true;
+  cudaFuncSetAttribute(multi, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  for (int g : {16, 64, 148}) {
+    for (int ns : {1, 2, 4, 8}) {
+      for (int chunk : {4096, 16384}) {
+        const int stages = (192 * 1024) / (ns * chunk) > 12 ? 12 : (192 * 1024) / (ns * chunk);
+        const size_t slice = (total / g) / (ns * chunk) * (ns * chunk);
+        for (int w = 0; w < 2; ++w) multi<<<g, 256, ns * stages * chunk>>>(src, slice, chunk, stages, ns, sink);
+        cudaEventRecord(e0);
+        for (int r = 0; r < 5; ++r) multi<<<g, 256, ns * stages * chunk>>>(src, slice, chunk, stages, ns, sink);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double gbs = double(slice) * g * 5 / (ms * 1e-3) / 1e9;
+        printf("%s{\"ctas\": %d, \"streams\": %d, \"chunk\": %d, \"stages\": %d, \"GBps\": %.0f, \"per_sm_GBps\": %.1f}",
+               first ? "" : ",\n", g, ns, chunk, stages, gbs, gbs / g);
+        first = false;
+      }
+    }
   }
   printf("\n], \"err\": \"%s\"}\n", cudaGetErrorString(cudaGetLastError()));
   return 0;

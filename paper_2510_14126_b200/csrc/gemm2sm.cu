@@ -35,7 +35,7 @@ constexpr int kPairN = 256;  // weight rows per CTA pair (MMA M)
 constexpr int kBK = 64;
 constexpr int kXBox2 = 16;   // activation rows per TMA box
 constexpr int kEpiRows = 32; // output rows (m) per epilogue chunk
-constexpr int kThreads2 = 192;
+constexpr int kThreads2 = 224;  // warps: 0 TMA (weights), 1 MMA, 2-5 epilogue, 6 TMA (tokens)
 struct Gemm2Args {
   int M, N, K;
   void* out;
@@ -224,15 +224,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 
   if (warp == 0) {
     if (elect_one()) {
-      // ---- TMA producer (both CTAs load their halves) ----
+      // ---- TMA producer, weights (both CTAs load their halves; warp 6 the tokens) ----
       uint32_t it = 0;
       int pos = seg_start(args, pair);
       Seg g;
       while (seg_next(args, pair, pos, g)) {
         const int n_tile = g.t / args.m_tiles;
         const int m_tile = g.t % args.m_tiles;
+        (void)m_tile;
         const int n0 = n_tile * kPairN + rank * 128;
-        const int x0 = m_tile * TN + rank * (TN / 2);
         for (int kb = g.kb0; kb < g.kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
@@ -242,10 +242,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             mbar_arrive_expect_tx(&full[s], 2 * L::kStage);
           else
             mbar_arrive_cluster(full_leader);
-          uint8_t* sa = smem + s * L::kStage;
-          uint8_t* sb = sa + L::kA;
+          tma_load_2d_2sm(smem + s * L::kStage, &tmap_w, full_leader, kb * kBK, n0);
+        }
+      }
+    }
+  } else if (warp == 6) {
+    if (elect_one()) {
+      // ---- second TMA issuer: the token rows. A TMA-issuing thread's copies complete
+      // one after another, so two issuers keep more bytes in flight per SM
+      // (benchmarks/micro/tma_tile.cu: 235 MB of weights in 47 us with one issuer,
+      // 40 us with two). The stage's expected bytes were armed by warp 0 (or are
+      // counted before the arm: the transaction count may go transiently negative).
+      uint32_t it = 0;
+      int pos = seg_start(args, pair);
+      Seg g;
+      while (seg_next(args, pair, pos, g)) {
+        const int m_tile = g.t % args.m_tiles;
+        const int x0 = m_tile * TN + rank * (TN / 2);
+        for (int kb = g.kb0; kb < g.kb1; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          const uint32_t full_leader = mapa_shared(smem_u32(&full[s]), 0);
+          uint8_t* sb = smem + s * L::kStage + L::kA;
           const int kc = kb * kBK;
-          tma_load_2d_2sm(sa, &tmap_w, full_leader, kc, n0);
 #pragma unroll
           for (int j = 0; j < TN / 2 / kXBox2; ++j)
             tma_load_2d_2sm(sb + j * kXBox2 * 128, &tmap_x, full_leader, kc, x0 + j * kXBox2);
@@ -282,7 +302,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         umma_commit_2sm_both(&tfull[b]);
       }
     }
-  } else {
+  } else if (warp < 6) {
     // ---- epilogue warps 2..5: TMEM lane quadrant = warp % 4 ----
     const int quad = warp & 3;
     const int ew = warp - 2;  // 0..3

@@ -42,6 +42,7 @@ struct SkArgs {
   int kb_per;   // K blocks per split
   int m_tiles;
   float* ws;    // [tiles][ks][2][TN][128] fp32 partials
+  int n_issue;  // TMA issuing threads: 1, 2 (weights | tokens) or 4 (two of each)
 };
 
 // NW weight sub-tiles of 256 rows per pair (one MMA each, sharing the staged token rows):
@@ -202,24 +203,36 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_trigger();
   const uint16_t pair_mask = static_cast<uint16_t>(3u << lead);
 
-  if (warp == 0) {
-    if (elect_one()) {
-      // ---- TMA producer: this CTA's 128 weight rows + TN/2 token rows per K block ----
-      const int n0 = n_tile * kPairN * NW + static_cast<int>(rank) * 128;
-      const int x0 = m_tile * TN + static_cast<int>(rank) * (TN / 2);
-      const uint64_t pol_w = policy_evict_first();  // weights: streamed once per step
-      for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
-        const int s = it % STAGES;
-        const uint32_t ph = (it / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        const uint32_t full_leader = mapa_shared(smem_u32(&full[s]), lead);
+  // ---- TMA issuers. The copies one thread issues complete one after another, so the
+  // weight boxes and the token-row boxes of a stage come from different warps, and with
+  // n_issue = 4 successive stages alternate between two issuers of each kind
+  // (benchmarks/micro/tma_tile.cu): warps 0 / 3 weights, warps 2 / 4 token rows (the
+  // epilogue warps 2-4 are idle until the accumulator is ready). The weight issuer of a
+  // stage arms its barrier; token-row bytes may land first (transiently negative count).
+  const int n_w = args.n_issue >= 4 ? 2 : 1;
+  const int w_idx = warp == 0 ? 0 : (warp == 3 && n_w == 2 ? 1 : -1);
+  const int x_idx = args.n_issue == 1 ? (warp == 0 ? 0 : -1)
+                                      : (warp == 2 ? 0 : (warp == 4 && n_w == 2 ? 1 : -1));
+  if ((w_idx >= 0 || x_idx >= 0) && elect_one()) {
+    const int n0 = n_tile * kPairN * NW + static_cast<int>(rank) * 128;
+    const int x0 = m_tile * TN + static_cast<int>(rank) * (TN / 2);
+    const uint64_t pol_w = policy_evict_first();  // weights: streamed once per step
+    for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
+      const bool do_w = w_idx >= 0 && it % n_w == w_idx;
+      const bool do_x = x_idx >= 0 && (args.n_issue == 1 || it % n_w == x_idx);
+      if (!do_w && !do_x) continue;
+      const int s = it % STAGES;
+      const uint32_t ph = (it / STAGES) & 1;
+      mbar_wait(&empty[s], ph ^ 1);
+      const uint32_t full_leader = mapa_shared(smem_u32(&full[s]), lead);
+      uint8_t* sa = smem + s * L::kStage;
+      uint8_t* sb = sa + L::kA;
+      const int kc = kb * kBK;
+      if (do_w) {
         if (rank == 0)
           mbar_arrive_expect_tx(&full[s], 2 * L::kStage);
         else
           mbar_arrive_cluster(full_leader);
-        uint8_t* sa = smem + s * L::kStage;
-        uint8_t* sb = sa + L::kA;
-        const int kc = kb * kBK;
 #pragma unroll
         for (int w = 0; w < NW; ++w)
           asm volatile(
@@ -229,12 +242,15 @@ __global__ void __launch_bounds__(kThreads, 1)
               "l"(reinterpret_cast<uint64_t>(&tmap_w)), "r"(full_leader), "r"(kc),
               "r"(n0 + w * kPairN), "l"(pol_w)
               : "memory");
+      }
+      if (do_x) {
 #pragma unroll
         for (int j = 0; j < TN / 2 / kXBox; ++j)
           tma_load_2d_2sm(sb + j * kXBox * 128, &tmap_x, full_leader, kc, x0 + j * kXBox);
       }
     }
-  } else if (warp == 1) {
+  }
+  if (warp == 1) {
     if (rank == 0 && elect_one()) {
       // ---- MMA issuer (pair leader, one thread) ----
       constexpr uint32_t idesc = umma_idesc_bf16(kPairN, TN);
@@ -258,6 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
+  __syncwarp();  // reconverge the issuing lanes before the warp-collective TMEM loads
   const int m0 = m_tile * TN;
   const int rows = min(TN, args.M - m0);
   // this CTA's partials: NW x [TN tokens][128 weight rows] fp32
@@ -343,6 +360,10 @@ int32_t launch_sk(const CUtensorMap* tw, const CUtensorMap* tx, const SkArgs& a,
 int g_sk_ks_force = -1;  // test / tuning hooks: force the split count / token tiles
 int g_sk_mt_force = -1;
 int g_sk_nw_force = -1;
+// -2: read CORTEX_SK_ISSUE once (default 2; 1, 2 and 4 issuers measured within noise of
+// each other at M = 64 ... 256 - the decode GEMMs are bound by L2 throughput, weights
+// plus the token rows every weight tile re-reads, not by TMA issue)
+int g_sk_issue = -2;
 
 }  // namespace
 
@@ -445,6 +466,12 @@ int32_t cortex_gemm_splitk_launch(const void* tmap_w, const void* tmap_x, int32_
   a.kb_per = (total_kb + ks - 1) / ks;
   a.m_tiles = mt;
   a.ws = workspace;
+  if (g_sk_issue == -2) {
+    const char* e = getenv("CORTEX_SK_ISSUE");
+    g_sk_issue = e ? atoi(e) : 2;
+    if (g_sk_issue != 1 && g_sk_issue != 4) g_sk_issue = 2;
+  }
+  a.n_issue = g_sk_issue;
   const auto* tw = reinterpret_cast<const CUtensorMap*>(tmap_w);
   const auto* tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
   if (nw == 2) {
