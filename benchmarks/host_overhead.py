@@ -30,7 +30,7 @@ def main(steps: int = 300) -> None:
     rt.run_steps(150)
     torch.cuda.synchronize()
     acc = {"blocked": 0.0, "forward": 0.0}
-    evts = w.meta_evt
+    evt_lists = [w.meta_evt, w.meta_evt_small]
 
     class TimedEvent:
         def __init__(self, e):
@@ -55,9 +55,10 @@ def main(steps: int = 300) -> None:
     w.forward = fwd
     t0 = time.perf_counter()
     for _ in range(steps):
-        for i, e in enumerate(evts):
-            if e is not None and not isinstance(e, TimedEvent):
-                evts[i] = TimedEvent(e)
+        for evts in evt_lists:
+            for i, e in enumerate(evts):
+                if e is not None and not isinstance(e, TimedEvent):
+                    evts[i] = TimedEvent(e)
         rt.step()
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0

@@ -80,6 +80,22 @@ int32_t cortex_table_copy(int32_t* table, int32_t table_stride, const int32_t* s
                           const int32_t* dst_rows, const int32_t* dst_cols,
                           const int32_t* counts, int32_t n, cortex_stream_t stream);
 
+/* Same three operations with the request arrays in HOST memory (plain int32 arrays,
+ * read during the call and passed to the kernel by value, in chunks of 256 requests for
+ * alloc / free and 128 for copies; allocation chunks are served in order). No staging
+ * copy precedes the kernel, so the allocator adds no copy-engine round trip to a step. */
+int32_t cortex_kv_alloc_h(uint32_t* bitmap, int32_t nblocks, int32_t id_base,
+                          const int32_t* counts, const int32_t* rows, const int32_t* cols,
+                          int32_t n_req, int32_t* table, int32_t table_stride, int32_t* status,
+                          cortex_stream_t stream);
+int32_t cortex_kv_free_h(uint32_t* bitmap, int32_t nblocks, int32_t id_base, const int32_t* table,
+                         int32_t table_stride, const int32_t* rows, const int32_t* cols,
+                         const int32_t* counts, int32_t n_req, int32_t* status,
+                         cortex_stream_t stream);
+int32_t cortex_table_copy_h(int32_t* table, int32_t table_stride, const int32_t* src_rows,
+                            const int32_t* dst_rows, const int32_t* dst_cols,
+                            const int32_t* counts, int32_t n, cortex_stream_t stream);
+
 /* Free-block count (occupancy metric; adds into *out_free). */
 int32_t cortex_kv_count_free(const uint32_t* bitmap, int32_t nblocks, int32_t* out_free,
                              cortex_stream_t stream);

@@ -27,6 +27,9 @@ SIGNATURES: dict[str, list] = {
     "cortex_kv_free": [P, I32, I32, P, I32, P, P, P, I32, P, P],
     "cortex_table_copy": [P, I32, P, P, P, P, I32, P],
     "cortex_kv_count_free": [P, I32, P, P],
+    "cortex_kv_alloc_h": [P, I32, I32, P, P, P, I32, P, I32, P, P],
+    "cortex_kv_free_h": [P, I32, I32, P, I32, P, P, P, I32, P, P],
+    "cortex_table_copy_h": [P, I32, P, P, P, P, I32, P],
     "cortex_tmap_encode_2d_bf16": [P, P, U64, U64, U64, ctypes.c_uint32, ctypes.c_uint32],
     "cortex_gemm_splits": [I32, I32, I32],
     "cortex_gemm_path": [I32, I32, I32],

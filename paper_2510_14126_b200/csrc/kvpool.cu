@@ -48,10 +48,9 @@ CORTEX_DEVICE int block_excl_scan(int v, int* smem, int* total) {
   return warp_base + incl - v;
 }
 
-__global__ void __launch_bounds__(kAllocThreads)
-    kv_alloc_kernel(uint32_t* bitmap, int nblocks, int id_base, const int* counts,
-                    const int* rows, const int* cols, int n_req, int* table, int table_stride,
-                    int* status) {
+CORTEX_DEVICE void kv_alloc_impl(uint32_t* bitmap, int nblocks, int id_base, const int* counts,
+                                 const int* rows, const int* cols, int n_req, int* table,
+                                 int table_stride, int* status) {
   __shared__ int s_off[kMaxReq + 1];
   __shared__ int s_scan[32];
   const int tid = threadIdx.x;
@@ -116,10 +115,38 @@ __global__ void __launch_bounds__(kAllocThreads)
   }
 }
 
+__global__ void __launch_bounds__(kAllocThreads)
+    kv_alloc_kernel(uint32_t* bitmap, int nblocks, int id_base, const int* counts,
+                    const int* rows, const int* cols, int n_req, int* table, int table_stride,
+                    int* status) {
+  kv_alloc_impl(bitmap, nblocks, id_base, counts, rows, cols, n_req, table, table_stride, status);
+}
+
+// Requests passed by value in the kernel parameters (the _h exports: host arrays, no
+// staging copy - an H2D copy before a kernel costs a copy-engine round trip of ~10-40 us
+// of GPU idle time per allocator call, profiles/r1_step_trace_pdl.txt).
+constexpr int kParamReq = 256;
+struct PoolReqs {
+  int n;
+  int a[kParamReq];
+  int b[kParamReq];
+  int c[kParamReq];
+};
+
+__global__ void __launch_bounds__(kAllocThreads)
+    kv_alloc_param_kernel(uint32_t* bitmap, int nblocks, int id_base,
+                          const __grid_constant__ PoolReqs r, int* table, int table_stride,
+                          int* status) {
+  pdl_wait();
+  pdl_trigger();
+  // a = counts, b = rows, c = cols
+  kv_alloc_impl(bitmap, nblocks, id_base, r.a, r.b, r.c, r.n, table, table_stride, status);
+}
+
 // Return blocks named by table[rows[i]][cols[i] .. cols[i]+counts[i]) to the pool.
-__global__ void kv_free_kernel(uint32_t* bitmap, int nblocks, int id_base, const int* table,
-                               int table_stride, const int* rows, const int* cols,
-                               const int* counts, int n_req, int* status) {
+CORTEX_DEVICE void kv_free_impl(uint32_t* bitmap, int nblocks, int id_base, const int* table,
+                                int table_stride, const int* rows, const int* cols,
+                                const int* counts, int n_req, int* status) {
   const int i = blockIdx.x;
   if (i >= n_req) return;
   const int c = counts[i];
@@ -136,6 +163,21 @@ __global__ void kv_free_kernel(uint32_t* bitmap, int nblocks, int id_base, const
   }
 }
 
+__global__ void kv_free_kernel(uint32_t* bitmap, int nblocks, int id_base, const int* table,
+                               int table_stride, const int* rows, const int* cols,
+                               const int* counts, int n_req, int* status) {
+  kv_free_impl(bitmap, nblocks, id_base, table, table_stride, rows, cols, counts, n_req, status);
+}
+
+__global__ void kv_free_param_kernel(uint32_t* bitmap, int nblocks, int id_base, const int* table,
+                                     int table_stride, const __grid_constant__ PoolReqs r,
+                                     int* status) {
+  pdl_wait();
+  pdl_trigger();
+  // a = rows, b = cols, c = counts
+  kv_free_impl(bitmap, nblocks, id_base, table, table_stride, r.a, r.b, r.c, r.n, status);
+}
+
 // table[dst_rows[i]][dst_cols[i] + k] = table[src_rows[i]][k], k < counts[i]
 __global__ void table_copy_kernel(int* table, int table_stride, const int* src_rows,
                                   const int* dst_rows, const int* dst_cols, const int* counts,
@@ -145,6 +187,25 @@ __global__ void table_copy_kernel(int* table, int table_stride, const int* src_r
   const int* src = table + static_cast<int64_t>(src_rows[i]) * table_stride;
   int* dst = table + static_cast<int64_t>(dst_rows[i]) * table_stride + dst_cols[i];
   for (int k = threadIdx.x; k < counts[i]; k += blockDim.x) dst[k] = src[k];
+}
+
+struct CopyReqs {
+  int n;
+  int src[kParamReq / 2];
+  int dst[kParamReq / 2];
+  int col[kParamReq / 2];
+  int cnt[kParamReq / 2];
+};
+
+__global__ void table_copy_param_kernel(int* table, int table_stride,
+                                        const __grid_constant__ CopyReqs r) {
+  pdl_wait();
+  pdl_trigger();
+  const int i = blockIdx.x;
+  if (i >= r.n) return;
+  const int* src = table + static_cast<int64_t>(r.src[i]) * table_stride;
+  int* dst = table + static_cast<int64_t>(r.dst[i]) * table_stride + r.col[i];
+  for (int k = threadIdx.x; k < r.cnt[i]; k += blockDim.x) dst[k] = src[k];
 }
 
 __global__ void popcount_kernel(const uint32_t* bitmap, int nwords, int* out_free) {
@@ -218,6 +279,71 @@ int32_t cortex_kv_count_free(const uint32_t* bitmap, int32_t nblocks, int32_t* o
   const int grid = (nwords + 255) / 256;
   popcount_kernel<<<grid < 148 ? grid : 148, 256, 0, stream>>>(bitmap, nwords, out_free);
   CORTEX_CHECK_LAUNCH();
+  return CORTEX_OK;
+}
+
+// Host-array variants: the request arrays are host memory, packed into the kernel
+// parameters (chunks of kParamReq requests, served in order).
+int32_t cortex_kv_alloc_h(uint32_t* bitmap, int32_t nblocks, int32_t id_base,
+                          const int32_t* counts, const int32_t* rows, const int32_t* cols,
+                          int32_t n_req, int32_t* table, int32_t table_stride, int32_t* status,
+                          cudaStream_t stream) {
+  if (!bitmap || nblocks <= 0 || n_req < 0 || !table || !status || (n_req && (!counts || !rows || !cols)))
+    return CORTEX_EBADARG;
+  for (int base = 0; base < n_req; base += kParamReq) {
+    PoolReqs r;
+    r.n = n_req - base < kParamReq ? n_req - base : kParamReq;
+    for (int i = 0; i < r.n; ++i) {
+      r.a[i] = counts[base + i];
+      r.b[i] = rows[base + i];
+      r.c[i] = cols[base + i];
+    }
+    if (pdl_launch(kv_alloc_param_kernel, 1, kAllocThreads, 0, stream, 1, bitmap, nblocks, id_base,
+                   r, table, table_stride, status) != cudaSuccess)
+      return CORTEX_ECUDA;
+  }
+  return CORTEX_OK;
+}
+
+int32_t cortex_kv_free_h(uint32_t* bitmap, int32_t nblocks, int32_t id_base, const int32_t* table,
+                         int32_t table_stride, const int32_t* rows, const int32_t* cols,
+                         const int32_t* counts, int32_t n_req, int32_t* status,
+                         cudaStream_t stream) {
+  if (!bitmap || nblocks <= 0 || n_req < 0 || !table || !status || (n_req && (!counts || !rows || !cols)))
+    return CORTEX_EBADARG;
+  for (int base = 0; base < n_req; base += kParamReq) {
+    PoolReqs r;
+    r.n = n_req - base < kParamReq ? n_req - base : kParamReq;
+    for (int i = 0; i < r.n; ++i) {
+      r.a[i] = rows[base + i];
+      r.b[i] = cols[base + i];
+      r.c[i] = counts[base + i];
+    }
+    if (pdl_launch(kv_free_param_kernel, r.n, 128, 0, stream, 1, bitmap, nblocks, id_base, table,
+                   table_stride, r, status) != cudaSuccess)
+      return CORTEX_ECUDA;
+  }
+  return CORTEX_OK;
+}
+
+int32_t cortex_table_copy_h(int32_t* table, int32_t table_stride, const int32_t* src_rows,
+                            const int32_t* dst_rows, const int32_t* dst_cols,
+                            const int32_t* counts, int32_t n, cudaStream_t stream) {
+  if (!table || n < 0 || (n && (!src_rows || !dst_rows || !dst_cols || !counts)))
+    return CORTEX_EBADARG;
+  for (int base = 0; base < n; base += kParamReq / 2) {
+    CopyReqs r;
+    r.n = n - base < kParamReq / 2 ? n - base : kParamReq / 2;
+    for (int i = 0; i < r.n; ++i) {
+      r.src[i] = src_rows[base + i];
+      r.dst[i] = dst_rows[base + i];
+      r.col[i] = dst_cols[base + i];
+      r.cnt[i] = counts[base + i];
+    }
+    if (pdl_launch(table_copy_param_kernel, r.n, 128, 0, stream, 1, table, table_stride, r) !=
+        cudaSuccess)
+      return CORTEX_ECUDA;
+  }
   return CORTEX_OK;
 }
 

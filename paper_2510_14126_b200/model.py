@@ -214,6 +214,13 @@ class GpuWorker:
                           for _ in range(self._ring)]
         self.meta_evt = [None] * self._ring
         self._meta_i = 0
+        # allocator / table-copy requests come in bursts (an admit is 2 uploads): their own
+        # deeper ring, so a burst never waits for the GPU to drain the previous step
+        self._ring_small = 64
+        self.meta_host_small = [torch.zeros(4 * 1024, dtype=torch.int32, pin_memory=True)
+                                for _ in range(self._ring_small)]
+        self.meta_evt_small = [None] * self._ring_small
+        self._meta_i_small = 0
         self.meta_dev = torch.zeros(self._meta_cap, dtype=torch.int32, device=dev)
         self.scale = 1.0 / math.sqrt(HEAD_DIM)
         self.launches = 0  # kernels of this library launched since construction
@@ -250,21 +257,27 @@ class GpuWorker:
         per_plane = self.n_blocks * self.cfg.n_kv_heads * BLOCK_TOKENS
         return (2 * layer) * per_plane, (2 * layer + 1) * per_plane
 
-    def _upload(self, arrays: list[np.ndarray], dev_buf: torch.Tensor | None = None
-                ) -> list[torch.Tensor]:
+    def _upload(self, arrays: list[np.ndarray], dev_buf: torch.Tensor | None = None,
+                small: bool = False) -> list[torch.Tensor]:
         """Stage int32 arrays through a pinned ring into `dev_buf` (one async H2D copy).
         A device buffer may be rewritten by the next upload: stream order guarantees
         the kernels that read it ran first."""
         dev_buf = self.meta_dev if dev_buf is None else dev_buf
         sizes = [a.size for a in arrays]
         total = sum(sizes)
-        if total > min(self._meta_cap, dev_buf.numel()):
+        hosts, evts = ((self.meta_host_small, self.meta_evt_small) if small
+                       else (self.meta_host, self.meta_evt))
+        if total > min(hosts[0].numel(), dev_buf.numel()):
             raise ValueError("step metadata exceeds staging capacity")
-        i = self._meta_i
-        self._meta_i = (i + 1) % self._ring
-        if self.meta_evt[i] is not None:
-            self.meta_evt[i].synchronize()
-        buf = self.meta_host[i]
+        if small:
+            i = self._meta_i_small
+            self._meta_i_small = (i + 1) % self._ring_small
+        else:
+            i = self._meta_i
+            self._meta_i = (i + 1) % self._ring
+        if evts[i] is not None:
+            evts[i].synchronize()
+        buf = hosts[i]
         host = buf.numpy()
         off = 0
         offs = []
@@ -275,35 +288,31 @@ class GpuWorker:
         dev_buf[:total].copy_(buf[:total], non_blocking=True)
         evt = torch.cuda.Event()
         evt.record()
-        self.meta_evt[i] = evt
+        evts[i] = evt
         self.h2d_bytes += 4 * total
         return [dev_buf[o:o + n] for o, n in zip(offs, sizes)]
 
     def upload_small(self, arrays: list[np.ndarray]) -> list[torch.Tensor]:
-        """Staging for allocator / table requests (separate device buffer)."""
-        return self._upload(arrays, self.meta_dev_small)
+        """Staging for allocator / table requests (separate device buffer and ring)."""
+        return self._upload(arrays, self.meta_dev_small, small=True)
+
+    # Block-pool requests travel in the kernel parameters (host arrays, the _h exports):
+    # no staging copy, so an admit adds no copy-engine round trip to the step.
 
     def alloc_blocks(self, pool, reqs: list[tuple[int, int, int]]) -> None:
         """Allocate from `pool` (an EngineSlice): reqs = (table row, first col, blocks)."""
-        counts, rows, cols = self.upload_small([
-            np.asarray([r[2] for r in reqs], np.int32), np.asarray([r[0] for r in reqs], np.int32),
-            np.asarray([r[1] for r in reqs], np.int32)])
-        ops.kv_alloc(pool.bitmap, pool.n_blocks, pool.block_base, counts, rows, cols, len(reqs),
-                     self.table, self.status)
-        self.launches += 1
+        ops.kv_alloc_h(pool.bitmap, pool.n_blocks, pool.block_base, [r[2] for r in reqs],
+                       [r[0] for r in reqs], [r[1] for r in reqs], self.table, self.status)
+        self.launches += (len(reqs) + 255) // 256
 
     def free_blocks(self, pool, reqs: list[tuple[int, int, int]]) -> None:
-        rows, cols, counts = self.upload_small([
-            np.asarray([r[0] for r in reqs], np.int32), np.asarray([r[1] for r in reqs], np.int32),
-            np.asarray([r[2] for r in reqs], np.int32)])
-        ops.kv_free(pool.bitmap, pool.n_blocks, pool.block_base, self.table, rows, cols, counts,
-                    len(reqs), self.status)
-        self.launches += 1
+        ops.kv_free_h(pool.bitmap, pool.n_blocks, pool.block_base, self.table,
+                      [r[0] for r in reqs], [r[1] for r in reqs], [r[2] for r in reqs],
+                      self.status)
+        self.launches += (len(reqs) + 255) // 256
 
     def copy_prefix_row(self, src_row: int, dst_row: int, n_blocks: int) -> None:
-        src, dst, col, cnt = self.upload_small([np.asarray([v], np.int32)
-                                                for v in (src_row, dst_row, 0, n_blocks)])
-        ops.table_copy(self.table, src, dst, col, cnt, 1)
+        ops.table_copy_h(self.table, [src_row], [dst_row], [0], [n_blocks])
         self.launches += 1
 
     def copy_first_token(self, src_row: int, dst_row: int) -> None:

@@ -321,3 +321,33 @@ def table_copy(table, src_rows, dst_rows, dst_cols, counts, n, stream=None) -> N
 def kv_count_free(bitmap, nblocks, out_free, stream=None) -> None:
     _check(lib().cortex_kv_count_free(bitmap.data_ptr(), nblocks, out_free.data_ptr(),
                                       _stream(stream)), "cortex_kv_count_free")
+
+
+def _hptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def _i32(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.int32))
+
+
+def kv_alloc_h(bitmap, nblocks, id_base, counts, rows, cols, table, status, stream=None) -> None:
+    """kv_alloc with the request arrays in host memory (passed in the kernel parameters)."""
+    c, r, k = _i32(counts), _i32(rows), _i32(cols)
+    _check(lib().cortex_kv_alloc_h(bitmap.data_ptr(), nblocks, id_base, _hptr(c), _hptr(r),
+                                   _hptr(k), len(c), table.data_ptr(), table.stride(0),
+                                   status.data_ptr(), _stream(stream)), "cortex_kv_alloc_h")
+
+
+def kv_free_h(bitmap, nblocks, id_base, table, rows, cols, counts, status, stream=None) -> None:
+    r, k, c = _i32(rows), _i32(cols), _i32(counts)
+    _check(lib().cortex_kv_free_h(bitmap.data_ptr(), nblocks, id_base, table.data_ptr(),
+                                  table.stride(0), _hptr(r), _hptr(k), _hptr(c), len(r),
+                                  status.data_ptr(), _stream(stream)), "cortex_kv_free_h")
+
+
+def table_copy_h(table, src_rows, dst_rows, dst_cols, counts, stream=None) -> None:
+    s, d, k, c = _i32(src_rows), _i32(dst_rows), _i32(dst_cols), _i32(counts)
+    _check(lib().cortex_table_copy_h(table.data_ptr(), table.stride(0), _hptr(s), _hptr(d),
+                                     _hptr(k), _hptr(c), len(s), _stream(stream)),
+           "cortex_table_copy_h")

@@ -503,7 +503,10 @@ def test_rope_kv_append(cuda):
 # ---------------------------------------------------------------- allocator
 
 
-def test_kv_alloc_free_matches_oracle(cuda):
+@pytest.mark.parametrize("host", [False, True])
+def test_kv_alloc_free_matches_oracle(cuda, host):
+    """Device-array requests (cortex_kv_alloc / _free) and host-array requests passed in
+    the kernel parameters (the _h exports the engine uses) against the pool oracle."""
     o = ops()
     nblocks, id_base, n_rows, stride = 1000, 5000, 40, 64
     ref = BlockPoolRef(nblocks, id_base)
@@ -522,8 +525,12 @@ def test_kv_alloc_free_matches_oracle(cuda):
             rows = rnd.sample(free_rows, k=min(len(free_rows), rnd.randint(1, 6)))
             counts = [rnd.choice([0, 1, 3, 16, 63]) for _ in rows]
             if sum(counts) > ref.n_free():
-                o.kv_alloc(bitmap, nblocks, id_base, dev(counts), dev(rows), dev([0] * len(rows)),
-                           len(rows), table, status)
+                if host:
+                    o.kv_alloc_h(bitmap, nblocks, id_base, counts, rows, [0] * len(rows), table,
+                                 status)
+                else:
+                    o.kv_alloc(bitmap, nblocks, id_base, dev(counts), dev(rows),
+                               dev([0] * len(rows)), len(rows), table, status)
                 torch.cuda.synchronize()
                 assert int(status[0]) == -3
                 status.zero_()
@@ -532,8 +539,11 @@ def test_kv_alloc_free_matches_oracle(cuda):
             for r, c, got in zip(rows, counts, ids):
                 held[r] = c
                 ref_table[r, :c] = got
-            o.kv_alloc(bitmap, nblocks, id_base, dev(counts), dev(rows), dev([0] * len(rows)),
-                       len(rows), table, status)
+            if host:
+                o.kv_alloc_h(bitmap, nblocks, id_base, counts, rows, [0] * len(rows), table, status)
+            else:
+                o.kv_alloc(bitmap, nblocks, id_base, dev(counts), dev(rows), dev([0] * len(rows)),
+                           len(rows), table, status)
         else:
             if not held:
                 continue
@@ -541,8 +551,11 @@ def test_kv_alloc_free_matches_oracle(cuda):
             counts = [held.pop(r) for r in rows]
             for r, c in zip(rows, counts):
                 ref.free(ref_table[r, :c].tolist())
-            o.kv_free(bitmap, nblocks, id_base, table, dev(rows), dev([0] * len(rows)), dev(counts),
-                      len(rows), status)
+            if host:
+                o.kv_free_h(bitmap, nblocks, id_base, table, rows, [0] * len(rows), counts, status)
+            else:
+                o.kv_free(bitmap, nblocks, id_base, table, dev(rows), dev([0] * len(rows)),
+                          dev(counts), len(rows), status)
         torch.cuda.synchronize()
         assert int(status[0]) == 0
         got_bitmap = bitmap.cpu().numpy().view(np.uint32)
@@ -553,6 +566,31 @@ def test_kv_alloc_free_matches_oracle(cuda):
     nfree = torch.zeros(1, dtype=torch.int32, device=cuda)
     o.kv_count_free(bitmap, nblocks, nfree)
     assert int(nfree[0]) == ref.n_free()
+
+
+def test_kv_host_requests_chunked(cuda):
+    """More requests than one kernel's parameter block holds (256): served in order over
+    several launches, identical to the oracle; table_copy_h copies rows."""
+    o = ops()
+    nblocks, n_req = 1200, 600
+    ref = BlockPoolRef(nblocks, 7)
+    bitmap = torch.from_numpy(ref.bitmap_words().view(np.int32)).to(cuda)
+    table = torch.full((n_req + 300, 4), -1, dtype=torch.int32, device=cuda)
+    status = torch.zeros(1, dtype=torch.int32, device=cuda)
+    counts = [1 + (i % 3) for i in range(n_req)]
+    counts = [c if sum(counts[:i + 1]) <= nblocks else 0 for i, c in enumerate(counts)]
+    ids = ref.alloc(counts)
+    o.kv_alloc_h(bitmap, nblocks, 7, counts, list(range(n_req)), [0] * n_req, table, status)
+    src = list(range(0, 300))
+    o.table_copy_h(table, src, [n_req + i for i in range(300)], [1] * 300, [2] * 300)
+    torch.cuda.synchronize()
+    assert int(status[0]) == 0
+    tab = table.cpu().numpy()
+    for r, (c, got) in enumerate(zip(counts, ids)):
+        assert tab[r, :c].tolist() == list(got)
+    for i in range(300):
+        assert tab[n_req + i, 1:3].tolist() == tab[i, :2].tolist()
+    assert np.array_equal(bitmap.cpu().numpy().view(np.uint32), ref.bitmap_words())
 
 
 def test_kv_double_free_flagged(cuda):
