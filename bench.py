@@ -392,6 +392,19 @@ def main() -> None:
                     kshare["launches"], 1), "launches": kshare["launches"],
                 "peak_source": peak_src + (" sustained" if bound == "tensor" else "")}
 
+    # every kernel class of the (untimed) profile window against both roofs; the
+    # attention window covers the side-stream tensor-core passes (cascade prefix +
+    # prompt prefill) overlapped with the HBM-bound per-call decode splits
+    rooflines = {}
+    for k, v in shares.items():
+        sec = max(v["ms"], 1e-9) / 1e3
+        gbs, tfs = v["bytes"] / sec / 1e9, v["flops"] / sec / 1e12
+        rooflines[k] = {"ms": v["ms"], "launches": v["launches"],
+                        "hbm_gbs": gbs, "hbm_frac": gbs / peaks["hbm_gbs"],
+                        "tflops": tfs, "tensor_frac": tfs / peaks["bf16_tflops_sustained"],
+                        "bytes_per_launch": v["bytes"] / max(v["launches"], 1),
+                        "flops_per_launch": v["flops"] / max(v["launches"], 1)}
+
     kv = _kv_stats(rt, kv_samples, cfg)
     line = {
         "metric": METRIC,
@@ -422,6 +435,7 @@ def main() -> None:
         "kernel_shares": {k: {"ms": v["ms"], "share": v["ms"] / prof_ms, "launches": v["launches"]}
                           for k, v in shares.items()},
         "roofline": roofline,
+        "rooflines_by_class": rooflines,
         "clocks": clk,
         "e2e": {"value": e2e_value, "unit": "workflows/s", "h2d_bytes_per_step": h2d / steps,
                 "d2h_bytes_per_step": d2h / steps},

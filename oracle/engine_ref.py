@@ -18,6 +18,9 @@ call, the block ids its row must hold (prefix blocks, then private blocks):
                          block, requests in batch order, one allocation per step
   complete_call(c)    -> catch-up to max(1, o), then free the private blocks
   evict_idle_prefix   -> free the stage's prefix blocks
+  retire (scale-in)   -> free every resident prefix (the engine is idle); a
+                         later engine on the recycled slice starts from an
+                         all-free pool (simulation.py:800-809)
 """
 
 from __future__ import annotations
@@ -86,6 +89,11 @@ class EngineBlocksRef:
         del self.calls[rid]
         return done
 
+    def retire(self) -> None:
+        assert not self.calls, "only idle engines retire (simulation.py:802-806)"
+        for sid in sorted(self.prefix):
+            self.evict(sid)
+
     def evict(self, sid: str) -> None:
         ids = self.prefix.pop(sid, None)
         if ids:
@@ -101,6 +109,8 @@ def replay_blocks(records, engine_blocks: dict[int, tuple[int, int]]) -> dict[in
     engines: dict[int, EngineBlocksRef] = {}
     for rec in records:
         eid = rec["eng"]
+        if rec["op"] == "create":
+            continue
         if eid not in engines:
             engines[eid] = EngineBlocksRef(*engine_blocks[eid])
         e = engines[eid]
@@ -121,6 +131,8 @@ def replay_blocks(records, engine_blocks: dict[int, tuple[int, int]]) -> dict[in
             e.complete(rid, order)
         elif op == "evict_idle_prefix":
             e.evict(rec["args"][0])
+        elif op == "retire":
+            e.retire()
     return engines
 
 

@@ -200,6 +200,7 @@ class GpuEngineState:
         self.prefill_tokens = 0
         self.blocks_in_use = 0
         self.peak_blocks = 0
+        self.closed = False  # set by close() (retired: the device slice was returned)
 
     # ------------------------------------------------------------------ views
 
@@ -338,14 +339,30 @@ class GpuEngineState:
                 self._free_prefix_rows.append(prefix.row)
 
     def close(self) -> None:
-        """Retire hook (the reference drops retired engines, simulation.py:806-809)."""
-        for call in list(self.batch):
-            self._gpu_release(call)
-        self.batch.clear()
-        for sid in list(self.resident):
-            p = self.resident.pop(sid)
+        """Retire hook: return every device block of this engine to its pool.
+
+        The reference retires an idle engine on autoscale scale-in by moving it to
+        `Simulator.retired_engines` (simulation.py:800-809) and has no hook for it;
+        the retired object's host accounting stays readable (the final report walks
+        retired engines, simulation.py:863), so only the device half is released:
+        the resident prefixes' blocks (and any in-flight call's private blocks)
+        go back to the bitmap, after which the slice can host a new engine.
+        Any later transition on this engine raises InternalInvariantViolation.
+        """
+        if self.closed:
+            return
+        for call in self.batch:
+            if call.priv_blocks:
+                self._free([(call.slot, _blocks(call.prefix_len), call.priv_blocks)])
+                call.priv_blocks = 0
+        for p in self.resident.values():
             if p.n_blocks:
                 self._free([(p.row, 0, p.n_blocks)])
+                p.n_blocks = 0
+        if self.blocks_in_use:
+            raise InternalInvariantViolation(
+                f"engine {self.engine_id}: {self.blocks_in_use} blocks unaccounted at close")
+        self.closed = True
 
     # ------------------------------------------------------------------ GPU mirror
 
@@ -383,7 +400,12 @@ class GpuEngineState:
                 start += m
             self.prefill_tokens += n
 
+    def _check_open(self) -> None:
+        if self.closed:
+            raise InternalInvariantViolation(f"engine {self.engine_id} was retired (closed)")
+
     def _gpu_admit(self, call: InFlightCall, prefix: ResidentPrefix, cold: bool) -> None:
+        self._check_open()
         w = self.worker
         P = prefix.tokens
         npb = _blocks(P)
@@ -420,6 +442,8 @@ class GpuEngineState:
 
     def _gpu_catch_up(self, targets: dict[int, int]) -> None:
         """Batched greedy decode steps until each call has its target token count."""
+        if self.closed and any(c.have < targets.get(id(c), 0) for c in self.batch):
+            self._check_open()
         while True:
             step = [c for c in self.batch if id(c) in targets and c.have < targets[id(c)]]
             if not step:

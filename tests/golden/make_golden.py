@@ -19,6 +19,13 @@ Fixtures
       pkg/tests/test_engines.py: demand, reservation, prefill time, decode
       progress, completion, eviction, LRU order, errors) with the reference's
       results after every call.
+  elastic/{dispatch,requests,kv_usage}.csv + summary.json + engine_calls.jsonl
+      + audit.json
+      the same NL2SQL trace with the reference's elastic policies on: borrowing
+      (simulation.py:715-763) and autoscale (:765-809) over isolated 1+3
+      engines, Poisson rate 2.0, 96 workflows (ELASTIC below). The call stream
+      adds "create" (autoscale scale-out / start-up) and "retire" (scale-in)
+      records; audit.json holds the reference's borrow / return / scale events.
   trace_seed0_{n}_pf{p}.json
       per-workflow stage/retry outcomes (prompt/output tokens per LLM visit,
       terminal, retries) for n workflows, computed by the reference Simulator.
@@ -162,6 +169,63 @@ def gen_config1() -> None:
         for rec in RecordingEngine.log:
             f.write(json.dumps(rec, sort_keys=True) + "\n")
     print("config1:", result.report.summary_line(), "calls:", len(RecordingEngine.log))
+
+
+ELASTIC = {"engines": (1, 3), "rate": 2.0, "cap": 96, "duration": 150.0,
+           "borrow": {"enabled": True, "util_low": 0.5, "util_high": 0.6},
+           "autoscale": {"enabled": True, "check_interval": 1.0, "cooldown": 8.0,
+                         "min_engines": 1, "max_engines": 4}}
+
+
+def elastic_config():
+    """Config-1 trace with borrowing + autoscale on (the ELASTIC parameters)."""
+    import dataclasses
+
+    from stagesim.scheduling import AutoscaleConfig, BorrowConfig
+
+    cfg = config1(engines=ELASTIC["engines"], duration=ELASTIC["duration"])
+    pol = ss.PolicyConfig(kind="slack", borrow=BorrowConfig(**ELASTIC["borrow"]),
+                          autoscale=AutoscaleConfig(**ELASTIC["autoscale"]))
+    return dataclasses.replace(cfg, policy=pol, arrival_rate=ELASTIC["rate"])
+
+
+class ElasticRecordingSimulator(CappedSimulator):
+    """Logs engine creation and retirement into RecordingEngine.log."""
+
+    engine_cls = RecordingEngine
+    cap = ELASTIC["cap"]
+
+    def _add_engine(self, pool_id, params):
+        engine = super()._add_engine(pool_id, params)
+        RecordingEngine.log.append({"eng": engine.engine_id, "op": "create",
+                                    "args": [pool_id, engine.last_advance],
+                                    "ret": None})
+        return engine
+
+    def _apply_scale(self, pool, decision):
+        before = set(self.retired_engines)
+        super()._apply_scale(pool, decision)
+        for eid in sorted(set(self.retired_engines) - before):
+            RecordingEngine.log.append({"eng": eid, "op": "retire", "args": [], "ret": None})
+
+
+def gen_elastic() -> None:
+    out = HERE / "elastic"
+    if out.exists():
+        shutil.rmtree(out)
+    RecordingEngine.log = []
+    sim = ElasticRecordingSimulator(elastic_config())
+    result = sim.run()
+    write_run_outputs(result, out)
+    with (out / "engine_calls.jsonl").open("w") as f:
+        for rec in RecordingEngine.log:
+            f.write(json.dumps(rec, sort_keys=True) + "\n")
+    a = sim.audit
+    audit = {"borrows": [list(x) for x in a.borrows], "returns": [list(x) for x in a.returns],
+             "scale_events": [list(x) for x in a.scale_events]}
+    (out / "audit.json").write_text(json.dumps(audit, sort_keys=True) + "\n")
+    print("elastic:", result.report.summary_line(), "calls:", len(RecordingEngine.log),
+          "borrows:", len(a.borrows), "scale events:", len(a.scale_events))
 
 
 def gen_traces() -> None:
@@ -312,4 +376,5 @@ def gen_engine_scenarios() -> None:
 if __name__ == "__main__":
     gen_engine_scenarios()
     gen_config1()
+    gen_elastic()
     gen_traces()

@@ -58,12 +58,23 @@ def _pending(d: dict, t: float) -> PendingCall:
                        d["target_output_tokens"])
 
 
-def replay_calls(records: list[dict], engines: dict) -> int:
-    """Drive engines with a reference call stream; returns the number of state checks."""
+def replay_calls(records: list[dict], engines: dict, factory=None, params=None) -> int:
+    """Drive engines with a reference call stream; returns the number of state checks.
+
+    With `factory` (integration.gpu_engine_factory), "create" records build the
+    engine and "retire" records close it and recycle its slice (the elastic run).
+    """
     checks = 0
     for i, rec in enumerate(records):
-        e = engines[rec["eng"]]
         op, args = rec["op"], rec["args"]
+        if op == "create":
+            engines[rec["eng"]] = factory(rec["eng"], params, args[0])
+            engines[rec["eng"]].last_advance = args[1]  # simulation.py:365
+            continue
+        if op == "retire":
+            factory.release(engines[rec["eng"]])
+            continue
+        e = engines[rec["eng"]]
         if op == "can_admit":
             got = e.can_admit(_pending(args[0], 0.0), args[1])
             assert got == rec["ret"], (i, rec)

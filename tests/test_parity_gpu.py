@@ -196,3 +196,74 @@ def test_reference_simulator_drives_gpu_engines(cuda, tmp_path):
     assert int(worker.status[0]) == 0
     for name in ("dispatch.csv", "requests.csv", "kv_usage.csv", "summary.json"):
         assert filecmp.cmp(tmp_path / name, GOLDEN / "config1" / name, shallow=False), name
+
+
+def test_elastic_reference_simulator_gpu(cuda, tmp_path):
+    """Borrowing + autoscale on the GPU: the reference Simulator
+    with its elastic policies on (tests/golden/elastic) drives GPU engines created on
+    scale-out and closed on scale-in; outputs byte-identical, block tables equal the
+    oracle's, retired slices return every block, borrowed calls' tokens match the
+    decoder oracle (the generator prefix re-materialised on a lent fixer engine)."""
+    if not _stagesim():
+        pytest.skip("reference package not importable on this box")
+    sys.path.insert(0, str(GOLDEN))
+    import json
+
+    from make_golden import ELASTIC as CFG
+    from make_golden import CappedSimulator, elastic_config
+    from stagesim.reporting import write_run_outputs
+
+    from paper_2510_14126_b200 import ops
+    from paper_2510_14126_b200.integration import gpu_engine_factory, gpu_simulator
+
+    golden = GOLDEN / "elastic"
+    worker = _worker(cuda, n_engines=6)
+    obs = RecordingObserver(read_device=True)
+    factory = gpu_engine_factory(worker, CONFIG1_PARAMS, seed=0, observer=obs)
+    sim = gpu_simulator(type("Cap", (CappedSimulator,), {"cap": CFG["cap"]}), factory)(
+        elastic_config())
+    result = sim.run()
+    write_run_outputs(result, tmp_path)
+    torch.cuda.synchronize()
+    assert int(worker.status[0]) == 0
+    for name in ("dispatch.csv", "requests.csv", "kv_usage.csv", "summary.json"):
+        assert filecmp.cmp(tmp_path / name, golden / name, shallow=False), name
+    audit = json.loads((golden / "audit.json").read_text())
+    assert [list(x) for x in sim.audit.borrows] == audit["borrows"]
+    assert [list(x) for x in sim.audit.scale_events] == audit["scale_events"]
+
+    records = load_jsonl(golden / "engine_calls.jsonl")
+    every = {**sim.retired_engines, **sim.engines}
+    ref = replay_blocks(records, {eid: (nb, b0) for eid, (b0, nb) in factory.assigned.items()})
+    n_calls = 0
+    for eid in sorted(every):
+        got, exp = obs.completed.get(eid, []), ref[eid].completed
+        assert [g["rid"] for g in got] == [e["rid"] for e in exp], eid
+        for g, e in zip(got, exp):
+            assert g["row"] == e["row"], (eid, g["rid"])
+            n_calls += 1
+    assert n_calls == 192
+    # device pools: each slice's free count = its blocks minus its current holder's
+    holders = {}
+    for eid, e in every.items():
+        if not e.closed:
+            holders[e.gpu.block_base] = e
+    for eid, e in every.items():
+        n_free = torch.zeros(1, dtype=torch.int32, device=cuda)
+        ops.kv_count_free(e.gpu.bitmap, e.gpu.n_blocks, n_free)
+        h = holders.get(e.gpu.block_base)
+        assert int(n_free[0]) == e.gpu.n_blocks - (h.blocks_in_use if h else 0), eid
+    # borrowed calls (generator stage on fixer engine 1): greedy tokens vs the decoder oracle
+    home = {r["eng"]: r["args"][0] for r in records if r["op"] == "create"}
+    borrowed = [c for c in obs.completed[1] if "pool:" + c["sid"] != home[1]][:3]
+    assert len(borrowed) == 3
+    dec = RefDecoder(TINY.to_ref(), worker.oracle_weights(), max_pos=4096)
+    for c in borrowed:
+        seq = dec.new_seq()
+        seq.extend(prefix_tokens(0, c["sid"], c["P"], TINY.vocab), "none")
+        logits = seq.extend(prompt_tokens(0, c["rid"], c["sid"], c["visit"], c["p"], TINY.vocab))
+        for k, t in enumerate(c["tokens"]):
+            if k:
+                logits = seq.extend([c["tokens"][k - 1]])
+            if greedy(logits) != t:
+                assert top2_margin(logits) < TIE_TOL, (c["rid"], k)
