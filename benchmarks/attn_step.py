@@ -80,7 +80,9 @@ def build(n_calls=215, n_pf=3, pf_len=200, slots=2, seed=0, layers=4):
     st["flat_plan"] = (d(plan[0]), plan[1], plan[2])
     st["flat_W"] = plan[2]
     st["flat"] = st["flat_plan"] if os.environ.get("CORTEX_FLAT_DECODE", "0") == "1" else None
-    persplit = max(ops.decode_splits(0, int(p)) for p in priv)
+    st["dzero"] = d([0] * n_calls)
+    persplit = max(max(ops.decode_splits(0, int(p)) for p in priv),
+                   max(ops.decode_splits(0, P + int(p)) for p in priv))
     st["max_splits"] = st["max_splits_cap"] = slots + max(persplit, plan[3], 8)
     st["o_part"] = torch.empty(n_calls * st["max_splits"] * HQ * 128, device=dev)
     st["lse"] = torch.empty(n_calls * st["max_splits"] * HQ, device=dev)
@@ -122,6 +124,28 @@ def decode_overlap(st, layer):
     st["ev"][1].record(st["side"])
     main.wait_event(st["ev"][1])
     decode(st, layer, 4)
+
+
+def decode_overlap_privfirst(st, layer):
+    """Private splits launched first (they fill the GPU), the cascade pass on the side
+    stream slots in as private CTAs retire."""
+    main = torch.cuda.current_stream()
+    st["ev"][0].record(main)
+    decode(st, layer, 2)
+    st["side"].wait_event(st["ev"][0])
+    decode(st, layer, 1, st["side"])
+    st["ev"][1].record(st["side"])
+    main.wait_event(st["ev"][1])
+    decode(st, layer, 4)
+
+
+def decode_nocascade(st, layer):
+    """No shared-prefix pass: every call's splits read its prefix too (from L2)."""
+    pl = st["plane"]
+    ops.paged_decode_attn(st["kvmap"], st["q"], st["table"], st["drow"], st["dzero"],
+                          st["dkv"], st["n_calls"], HKV, GROUP, 2 * layer * pl,
+                          (2 * layer + 1) * pl, 1 / math.sqrt(128), st["o_part"], st["lse"],
+                          st["max_splits"], st["attn"])
 
 
 def layer_side_prefill(st, layer):
@@ -190,6 +214,8 @@ def main():
         "combine_us": timed(st, lambda l: decode(st, l, 4)),
         "decode_serial_us": timed(st, lambda l: decode(st, l, 7)),
         "decode_overlap_us": timed(st, lambda l: decode_overlap(st, l)),
+        "decode_overlap_privfirst_us": timed(st, lambda l: decode_overlap_privfirst(st, l)),
+        "decode_nocascade_us": timed(st, lambda l: decode_nocascade(st, l)),
         "prefill_us": timed(st, lambda l: prefill(st, l)),
         "layer_us": timed(st, lambda l: (decode_overlap(st, l), prefill(st, l))),
         "layer_side_prefill_us": timed(st, lambda l: layer_side_prefill(st, l)),

@@ -438,7 +438,10 @@ CORTEX_DEVICE void dec_merge_emit(const float* cm, const float* cl, const float*
     for (int w = 0; w < kWarps; ++w) M = fmaxf(M, cm[w * 8 + r]);
     float L = 0.f, O = 0.f;
     for (int w = 0; w < kWarps; ++w) {
-      const float f = cm[w * 8 + r] == -INFINITY ? 0.f : exp2f(cm[w * 8 + r] - M);
+      // a warp without keys (a split shorter than 4 tiles) left its O rows unwritten
+      // (stale stage bytes, possibly NaN patterns): skip it rather than scale it by 0
+      if (cm[w * 8 + r] == -INFINITY) continue;
+      const float f = exp2f(cm[w * 8 + r] - M);
       L += cl[w * 8 + r] * f;
       O += co[(w * co_rows + r) * kHeadDim + d] * f;
     }

@@ -275,8 +275,11 @@ def _logical_kv(cache, layer, table_row, prefix, kvlen):
 
 def _seq_specs(rng, nb, max_blocks):
     # (prefix_len, kv_len) cases: no prefix, aligned prefix, ragged prefix, long
+    # (0, 513) / (0, 545) / (1000, 1000 + 513 ...): a last split of 1-3 tiles, so some of
+    # the CTA's 4 warps own no key at all (their merge rows must be skipped, not scaled)
     specs = [(0, 1), (0, 17), (40, 41), (40, 77), (1000, 1000 + 137), (16, 300), (5, 5 + 256),
-             (0, 255), (0, 256), (0, 257), (1000, 1000 + 700)]
+             (0, 255), (0, 256), (0, 257), (1000, 1000 + 700), (0, 513), (0, 545),
+             (1000, 1000 + 1050)]
     tables = []
     perm = rng.permutation(nb)
     used = 0
@@ -292,7 +295,7 @@ def _seq_specs(rng, nb, max_blocks):
 @pytest.mark.parametrize("flat", [False, True])
 def test_paged_decode_attention(cuda, group, flat):
     o = ops()
-    hkv, L, nb, max_blocks = 2, 2, 512, 128
+    hkv, L, nb, max_blocks = 2, 2, 640, 134
     hq = hkv * group
     cache = _make_cache(cuda, L, nb, hkv, seed=11 + group)
     rng = np.random.default_rng(5)
@@ -356,7 +359,8 @@ def test_cascade_decode_attention(cuda, group, plens, impl):
     for g, P in enumerate(plens):
         first = len(seq_row)
         for i in range(counts[g]):
-            priv = int(rng.integers(1, 300))
+            # ragged private lengths, some past one 512-token split (a 1-3 tile 2nd split)
+            priv = int(rng.integers(1, 300)) if i % 3 else int(rng.integers(513, 560))
             npr = (priv + 15) // 16
             ids = pref_blocks[g] + [perm.pop() for _ in range(npr)]
             table[r, :len(ids)] = torch.tensor(ids, dtype=torch.int32)
@@ -370,7 +374,7 @@ def test_cascade_decode_attention(cuda, group, plens, impl):
     dev = lambda a: torch.as_tensor(np.asarray(a, dtype=np.int32), device=cuda)
     table = table.to(cuda)
     pslots = max([((P + 15) // 16 + 15) // 16 for _, P, _, _ in grp] + [1])
-    priv = max(((kv - p) + 255) // 256 for p, kv in zip(seq_pre, seq_kv))
+    priv = max(o.decode_splits(0, kv - p) for p, kv in zip(seq_pre, seq_kv))
     max_splits = pslots + priv
     plan = None
     if impl == "tc-flat":

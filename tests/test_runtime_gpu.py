@@ -83,3 +83,57 @@ def test_runtime_outcomes_and_tokens(cuda, mode):
                 assert top2_margin(logits) < 2e-2
     assert n_tok > 1000
     assert mism <= max(3, n_tok // 500)
+
+
+def test_runtime_long_prefix_config4(cuda):
+    """BASELINE config 4's shape on the tiny decoder: 8K-token schema prefixes and 512-token
+    outputs, so private contexts pass one 512-token decode split (a short 2nd split) and the
+    8K prefix is chunk-prefilled and reused across retries. Outcomes equal the reference
+    trace; SQL of a first call and a retry match the CPU oracle; logits stay finite."""
+    from paper_2510_14126_b200.workflow import Constant
+
+    n, conc, P = 8, 8, 8192
+    spec = Nl2Sql(retry_budget=5, generator_prefix_tokens=P, fixer_prefix_tokens=P,
+                  output_tokens=Constant(512), executor_service_time=Uniform(0.001, 0.004))
+    max_seq = P + 300 + 512
+    params = EngineParams(P + conc * 812, 5000.0, 0.02, 0.1, conc)
+    bpe = blocks_for(params)
+    worker = GpuWorker(TINY, cuda, n_blocks=2 * bpe, n_rows=2 * (conc + 4),
+                       row_cols=(max_seq + 15) // 16 + 2, max_tokens=2048, max_out=2 * conc + 16,
+                       hist_cols=520, max_seq_tokens=max_seq + 16)
+    rt = PoolRuntime(worker, spec, params, mode="isolated", concurrency=conc, n_workflows=n,
+                     prefill_budget=1500)
+    results = []
+    rt.on_result = lambda call, toks: results.append((call.request_id, call.stage_id, call.visit,
+                                                     call.prompt_tokens, toks))
+    finite = []
+    worker.on_forward = lambda plan, n_out: finite.append(
+        bool(torch.isfinite(worker.logits[:n_out]).all()))
+    rt.fill()
+    rt.run_until(n, max_seconds=600)
+    torch.cuda.synchronize()
+    assert int(worker.status[0]) == 0
+    assert all(finite)
+    gold = {w["rid"]: w for w in json.loads((GOLDEN / "trace_seed0_64_pf5.json").read_text())
+            ["workflows"]}
+    got = {wf.rid: wf for wf in rt.finished}
+    assert sorted(got) == list(range(n))
+    for rid, wf in got.items():
+        assert wf.terminal == gold[rid]["terminal"]
+        assert [h[0] for h in wf.history] == gold[rid]["stages"]
+    assert all(len(t) == 512 for *_, t in results)
+    dec = RefDecoder(TINY.to_ref(), worker.oracle_weights(), max_pos=max_seq + 16)
+    picks = [results[0]] + [r for r in results if r[1] != results[0][1]][:1]
+    mism = n_tok = 0
+    for rid, sid, visit, p, toks in picks:
+        seq = dec.new_seq()
+        seq.extend(prefix_tokens(0, sid, P, TINY.vocab), "none")
+        logits = seq.extend(prompt_tokens(0, rid, sid, visit, p, TINY.vocab))
+        for k, t in enumerate(toks):
+            if k:
+                logits = seq.extend([int(toks[k - 1])])
+            n_tok += 1
+            if greedy(logits) != int(t):
+                mism += 1
+                assert top2_margin(logits) < 2e-2, (rid, sid, k)
+    assert n_tok == 1024 and mism <= 3
