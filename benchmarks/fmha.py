@@ -108,9 +108,11 @@ def cascade(prefix: int, n_calls: int, groups: int = 2) -> dict:
 
 
 if __name__ == "__main__":
-    print(json.dumps(prefill(1000, [200] * 2)), flush=True)
-    print(json.dumps(prefill(1000, [200] * 8)), flush=True)
-    print(json.dumps(prefill(0, [1000])), flush=True)
-    print(json.dumps(prefill(0, [8192])), flush=True)
-    print(json.dumps(cascade(1000, 115)), flush=True)
-    print(json.dumps(cascade(8192, 128)), flush=True)
+    # both tcgen05 kernels: two Q tiles per CTA (default) and one
+    for q2 in (1, 0, -1):
+        ops.fmha_set_2q(q2)
+        for r in (prefill(1000, [200] * 2), prefill(1000, [200] * 8), prefill(0, [1000]),
+                  prefill(0, [8192]), cascade(1000, 115), cascade(8192, 128)):
+            r["q_tiles_per_cta"] = {1: 2, 0: 1, -1: "auto"}[q2]
+            print(json.dumps(r), flush=True)
+    ops.fmha_set_2q(-1)

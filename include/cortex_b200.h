@@ -232,10 +232,13 @@ int32_t cortex_paged_decode_attn_flat(
 int32_t cortex_tmap_encode_q(void* tmap_out, const void* q, uint64_t n_tok, int32_t hq,
                              int32_t group);
 
-/* tcgen05 flash attention, 128 query rows (tokens x GQA group) per CTA, paged K/V in
+/* tcgen05 flash attention, 2 x 128 query rows (tokens x GQA group) per CTA (two Q tiles
+ * ping-ponging softmax against the MMAs, chosen per launch by wave count;
+ * cortex_fmha_set_2q(-1 auto | 0 one tile | 1 two tiles)), paged K/V in
  * 8-block key tiles, TMEM S/O accumulators. Prefill: same contract as
  * cortex_paged_prefill_attn. Cascade: the shared-prefix pass of decode (partials into
  * slots [0, prefix_slots) of o_part / lse_part, rows = decode index). */
+int32_t cortex_fmha_set_2q(int32_t on);
 int32_t cortex_fmha_prefill_tc(const void* tmap_kv, const void* tmap_q, void* out,
                                const int32_t* table, int32_t table_stride, const int32_t* seq_row,
                                const int32_t* seq_prefix, const int32_t* seq_kvlen,

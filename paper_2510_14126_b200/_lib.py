@@ -57,6 +57,7 @@ SIGNATURES: dict[str, list] = {
     "cortex_paged_decode_attn_flat": [P, P, P, I32, P, P, P, P, I32, I32, I32, I32, I32, I64, I64,
                                       F32, P, P, I32, P, P, P, P, P, I32, I32, I32, P, I32, P],
     "cortex_tmap_encode_q": [P, P, U64, I32, I32],
+    "cortex_fmha_set_2q": [I32],
     "cortex_fmha_prefill_tc": [P, P, P, P, I32, P, P, P, P, P, I32, I32, I32, I32, I64, I64, F32,
                                P],
     "cortex_fmha_cascade_tc": [P, P, P, I32, P, P, P, P, I32, I32, I32, I32, I32, I64, I64, F32,

@@ -555,6 +555,367 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Two-Q-tile variant (ping-pong): one CTA owns 2 x 128 query rows (Q tiles A and B,
+// 2 x tpb tokens) and streams every K/V tile once for both, so the L2 -> SM traffic per
+// flop halves, and the tensor pipe computes one tile's S / PV while the other tile's
+// softmax runs:
+//   MMA warp: S_A(0) S_B(0) | PV_A(t) S_A(t+1) PV_B(t) S_B(t+1) | ...
+//   softmax warpgroup A (warps 2-5) and B (warps 6-9): one thread per query row, all
+//   128 keys of the tile (no cross-warp max exchange), lazy O rescale, P -> TMEM.
+// TMEM: S_A [0,128)  S_B [128,256)  O_A [256,384)  O_B [384,512) (S single-buffered per
+// tile: S_X(t+1) is issued after PV_X(t), which consumed P_X(t) in place, in MMA order).
+// Smem: Q_A 32 KiB, Q_B 32 KiB, 2 K/V stages of 64 KiB, barriers.
+constexpr int kOffQ2 = 0;
+constexpr int kOffKV2 = 2 * kQBytes;
+constexpr int kOffBar2 = kOffKV2 + kStagesTC * kKVStage;
+constexpr int kSmemTC2 = kOffBar2 + 256 + 1024;
+
+__global__ void __launch_bounds__(kThreadsTC, 1)
+    fmha2_tc_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                    const __grid_constant__ CUtensorMap tmap_kv, const FmhaArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar2);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;   // [2]
+  uint64_t* k_empty = bars + 3;  // [2]
+  uint64_t* v_full = bars + 5;   // [2]
+  uint64_t* v_empty = bars + 7;  // [2]
+  uint64_t* s_full = bars + 9;   // [2 tiles]
+  uint64_t* p_full = bars + 11;  // [2 tiles]
+  uint64_t* o_ready = bars + 13; // [2 tiles] committed after every PV of the tile
+  uint64_t* o_done = bars + 15;  // [2 tiles]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 17);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int qb = blockIdx.x;  // pair of Q tiles
+  const int kvh = blockIdx.y;
+  const int item = blockIdx.z;
+  const int group = a.group;
+  const int tpb = kRows / group;  // query tokens per tile
+
+  // ---- work item (as fmha_tc_kernel, over 2 tpb tokens) ----
+  int row, prefix_len, kv_len, tok0, ntok, qpos_base, blk_begin, blk_end;
+  if (a.mode == 0) {
+    const int qlen = __ldg(&a.seq_qlen[item]);
+    if (qb * 2 * tpb >= qlen) return;
+    row = __ldg(&a.seq_row[item]);
+    prefix_len = __ldg(&a.seq_prefix[item]);
+    kv_len = __ldg(&a.seq_kvlen[item]);
+    tok0 = __ldg(&a.seq_qstart[item]) + qb * 2 * tpb;
+    ntok = min(2 * tpb, qlen - qb * 2 * tpb);
+    qpos_base = kv_len - qlen + qb * 2 * tpb;
+    const int last = qpos_base + ntok - 1;
+    const int npb = (prefix_len + kBlk - 1) / kBlk;
+    blk_begin = 0;
+    blk_end = last < prefix_len ? last / kBlk + 1 : npb + (last - prefix_len) / kBlk + 1;
+  } else {
+    const int g = item / a.max_psplits;
+    const int ps = item % a.max_psplits;
+    const int count = __ldg(&a.grp_count[g]);
+    if (qb * 2 * tpb >= count) return;
+    row = __ldg(&a.grp_row[g]);
+    prefix_len = __ldg(&a.grp_plen[g]);
+    kv_len = prefix_len;
+    const int npb = (prefix_len + kBlk - 1) / kBlk;
+    const int psb = prefix_split_blocks(npb, a.max_psplits);
+    blk_begin = ps * psb;
+    if (blk_begin >= npb) return;
+    blk_end = min(npb, blk_begin + psb);
+    tok0 = __ldg(&a.grp_first[g]) + qb * 2 * tpb;
+    ntok = min(2 * tpb, count - qb * 2 * tpb);
+    qpos_base = 0x3fffffff;
+  }
+  const bool has_b = ntok > tpb;  // CTA-uniform: tile B holds at least one token
+  const int n_kt = (blk_end - blk_begin + kBlocksPerTile - 1) / kBlocksPerTile;
+  const int* table_row = a.table + static_cast<int64_t>(row) * a.table_stride;
+  const int hq = a.n_kv_heads * group;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_q);
+    tma_prefetch_desc(&tmap_kv);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < kStagesTC; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(&s_full[x], 1);
+      mbar_init(&p_full[x], 4);
+      mbar_init(&o_ready[x], 1);
+      mbar_init(&o_done[x], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_holder, kTmemColsTC);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      // ---- producer ----
+      mbar_arrive_expect_tx(q_full, (has_b ? 2 : 1) * kQBytes);
+      for (int x = 0; x < (has_b ? 2 : 1); ++x) {
+        uint8_t* qd = smem + kOffQ2 + x * kQBytes;
+        tma_load_3d(qd, &tmap_q, q_full, 0, kvh * group, tok0 + x * tpb);
+        tma_load_3d(qd + kQBytes / 2, &tmap_q, q_full, 64, kvh * group, tok0 + x * tpb);
+      }
+      for (int kt = 0; kt < n_kt; ++kt) {
+        const int s = kt % kStagesTC;
+        const uint32_t ph = (kt / kStagesTC) & 1;
+        uint8_t* st = smem + kOffKV2 + s * kKVStage;
+        int rows[kBlocksPerTile];
+#pragma unroll
+        for (int j = 0; j < kBlocksPerTile; ++j) {
+          const BlockRef b = block_ref(table_row, prefix_len, kv_len,
+                                       blk_begin + kt * kBlocksPerTile + j, blk_end);
+          rows[j] = static_cast<int>((static_cast<int64_t>(b.block) * a.n_kv_heads + kvh) * kBlk);
+        }
+        mbar_wait_guard(&k_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&k_full[s], 2 * kKVHalf);
+#pragma unroll
+        for (int j = 0; j < kBlocksPerTile; ++j) {
+          const int off = j * kBlk * 128;
+          tma_load_2d(st + 0 * kKVHalf + off, &tmap_kv, &k_full[s], 0, static_cast<int>(a.k_row0) + rows[j]);
+          tma_load_2d(st + 1 * kKVHalf + off, &tmap_kv, &k_full[s], 64, static_cast<int>(a.k_row0) + rows[j]);
+        }
+        mbar_wait_guard(&v_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&v_full[s], 2 * kKVHalf);
+#pragma unroll
+        for (int j = 0; j < kBlocksPerTile; ++j) {
+          const int off = j * kBlk * 128;
+          tma_load_2d(st + 2 * kKVHalf + off, &tmap_kv, &v_full[s], 0, static_cast<int>(a.v_row0) + rows[j]);
+          tma_load_2d(st + 3 * kKVHalf + off, &tmap_kv, &v_full[s], 64, static_cast<int>(a.v_row0) + rows[j]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      // ---- MMA issuer ----
+      constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128);
+      constexpr uint32_t idesc_pv = umma_idesc_bf16(128, 128) | (1u << 16);  // V MN-major
+      const int nx = has_b ? 2 : 1;
+      mbar_wait_guard(q_full, 0);
+      auto issue_s = [&](int kt, int x) {
+        const int s = kt % kStagesTC;
+        const uint32_t q_addr = smem_u32(smem + kOffQ2 + x * kQBytes);
+        const uint32_t k_addr = smem_u32(smem + kOffKV2 + s * kKVStage);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * kKVHalf + (kk & 3) * 32;
+          umma_bf16_ss(tmem + 128 * x, umma_desc_sw128(q_addr + off),
+                       umma_desc_sw128(k_addr + off), idesc_s, kk != 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[x]);
+      };
+      auto issue_pv = [&](int kt, int x) {
+        const int s = kt % kStagesTC;
+        const uint32_t v_addr = smem_u32(smem + kOffKV2 + s * kKVStage + 2 * kKVHalf);
+        const uint32_t p_tmem = tmem + 128 * x;
+        const uint32_t o_tmem = tmem + 256 + 128 * x;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          umma_bf16_ts(o_tmem, p_tmem + 8 * kk, umma_desc_sw128_mn(v_addr + kk * 2048, kKVHalf),
+                       idesc_pv, (kt | kk) != 0 ? 1u : 0u);
+        }
+        umma_commit(&o_ready[x]);
+        if (kt == n_kt - 1) umma_commit(&o_done[x]);
+      };
+      if (n_kt > 0) {
+        mbar_wait_guard(&k_full[0], 0);
+        tc_fence_after();
+        for (int x = 0; x < nx; ++x) issue_s(0, x);
+        umma_commit(&k_empty[0]);
+      }
+      for (int kt = 0; kt < n_kt; ++kt) {
+        const int s = kt % kStagesTC;
+        const bool more = kt + 1 < n_kt;
+        const int s1 = (kt + 1) % kStagesTC;
+        mbar_wait_guard(&v_full[s], (kt / kStagesTC) & 1);
+        for (int x = 0; x < nx; ++x) {
+          mbar_wait_guard(&p_full[x], kt & 1);
+          tc_fence_after();
+          issue_pv(kt, x);
+          if (more) {  // S_x(kt+1) right behind PV_x(kt), while the other tile's softmax runs
+            if (x == 0) {
+              mbar_wait_guard(&k_full[s1], ((kt + 1) / kStagesTC) & 1);
+              tc_fence_after();
+            }
+            issue_s(kt + 1, x);
+          }
+        }
+        umma_commit(&v_empty[s]);
+        if (more) umma_commit(&k_empty[s1]);
+      }
+    }
+  } else {
+    // ---- softmax: warpgroup x = tile (warps 2-5 tile A, 6-9 tile B); thread <-> row ----
+    const int x = (warp - 2) >> 2;
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    if (x == 1 && !has_b) goto done;
+    {
+      const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+      const uint32_t tmem_s = tmem + 128 * x;
+      const uint32_t tmem_o = tmem + 256 + 128 * x;
+      const int ntok_x = min(tpb, ntok - x * tpb);
+      const bool row_ok = r < ntok_x * group;
+      const int qpos0 = qpos_base == 0x3fffffff ? qpos_base : qpos_base + x * tpb;
+      const int qpos = qpos0 == 0x3fffffff ? qpos0 : qpos0 + r / group;
+      float m_run = -INFINITY, l_run = 0.f;
+      for (int kt = 0; kt < n_kt; ++kt) {
+        mbar_wait_guard(&s_full[x], kt & 1);
+        tc_fence_after();
+        // keys [0, 64) stay in registers; keys [64, 128) are read twice from TMEM (max,
+        // then exp) to keep the thread at 64 live scores (168-register budget)
+        const int j0 = blk_begin + kt * kBlocksPerTile;
+        // fast path (tile-uniform): every key valid and visible to every row of the tile
+        bool full = j0 + kBlocksPerTile <= blk_end;
+#pragma unroll
+        for (int j = 0; j < kBlocksPerTile; ++j) {
+          const BlockSpan b = block_span(prefix_len, kv_len, j0 + j, blk_end);
+          full = full && b.nvalid == kBlk && b.pos0 + kBlk - 1 <= qpos0;
+        }
+        // masks the 64 scores of key half h in place (invalid / causal / padding rows)
+        auto mask_half = [&](float (&v)[64], int h) {
+#pragma unroll
+          for (int j = 0; j < kBlocksPerTile / 2; ++j) {
+            const BlockSpan b = block_span(prefix_len, kv_len, j0 + 4 * h + j, blk_end);
+#pragma unroll
+            for (int i = 0; i < kBlk; ++i) {
+              const bool ok = row_ok && i < b.nvalid && b.pos0 + i <= qpos;
+              v[kBlk * j + i] = ok ? v[kBlk * j + i] : -INFINITY;
+            }
+          }
+        };
+        auto load_half = [&](float (&v)[64], int h) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            uint32_t u[32];
+            tmem_ld_x32(tmem_s + lane_off + 64 * h + 32 * c, u);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[32 * c + i] = __uint_as_float(u[i]);
+          }
+          if (!full) mask_half(v, h);
+        };
+        float sv[64];
+        float mraw = -INFINITY;
+        load_half(sv, 1);
+#pragma unroll
+        for (int i = 0; i < 64; ++i) mraw = fmaxf(mraw, sv[i]);
+        load_half(sv, 0);
+#pragma unroll
+        for (int i = 0; i < 64; ++i) mraw = fmaxf(mraw, sv[i]);
+        const float mt = mraw * a.scale_log2;
+        const bool adopt = mt > -INFINITY && (m_run == -INFINITY || mt > m_run + kRescaleThresh);
+        const float alpha = !adopt ? 1.f : (m_run == -INFINITY ? 0.f : exp2f(m_run - mt));
+        const float m_new = adopt ? mt : m_run;
+        const float m_use = m_new == -INFINITY ? 0.f : m_new;
+        if (kt > 0 && __any_sync(0xffffffffu, adopt && m_run != -INFINITY)) {
+          mbar_wait_guard(&o_ready[x], (kt - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t u[32];
+            tmem_ld_x32(tmem_o + lane_off + 32 * c, u);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * alpha);
+            tmem_st_x32(tmem_o + lane_off + 32 * c, u);
+          }
+          tmem_st_wait();
+        }
+        // p = exp2(s * scale - m); P as bf16 (keys 2c / 2c+1 packed in column c) over S
+        // columns [0, 64): half 0's P lands on S columns already consumed, half 1's
+        // scores (S columns [64, 128)) are re-read before any P column reaches them.
+        // (P hi + lo is the one-tile kernel's option.)
+        float lsum = 0.f;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h == 1) load_half(sv, 1);
+#pragma unroll
+          for (int i = 0; i < 64; ++i) {
+            sv[i] = ex2_approx(fmaf(sv[i], a.scale_log2, -m_use));
+            lsum += sv[i];
+          }
+          uint32_t hi[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) hi[c] = pack_bf16(sv[2 * c], sv[2 * c + 1]);
+          tmem_st_x32(tmem_s + lane_off + 32 * h, hi);
+        }
+        l_run = l_run * alpha + lsum;
+        m_run = m_new;
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[x]);
+      }
+      // ---- epilogue: this tile's O rows ----
+      mbar_wait_guard(&o_done[x], 0);
+      tc_fence_after();
+      const int tok = tok0 + x * tpb + r / group;
+      const int h = kvh * group + r % group;
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+      if (a.mode == 0) {
+        __nv_bfloat16* orow = a.out + (static_cast<int64_t>(tok) * hq + h) * kHD;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t u[32];
+          tmem_ld_x32(tmem_o + lane_off + 32 * c, u);
+          tmem_ld_wait();
+          if (row_ok) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              uint4 v;
+              v.x = pack_bf16(__uint_as_float(u[i]) * inv, __uint_as_float(u[i + 1]) * inv);
+              v.y = pack_bf16(__uint_as_float(u[i + 2]) * inv, __uint_as_float(u[i + 3]) * inv);
+              v.z = pack_bf16(__uint_as_float(u[i + 4]) * inv, __uint_as_float(u[i + 5]) * inv);
+              v.w = pack_bf16(__uint_as_float(u[i + 6]) * inv, __uint_as_float(u[i + 7]) * inv);
+              *reinterpret_cast<uint4*>(orow + 32 * c + i) = v;
+            }
+          }
+        }
+      } else {
+        const int ps = item % a.max_psplits;
+        const int64_t pidx = (static_cast<int64_t>(tok) * a.max_splits + ps) * hq + h;
+        float* o = a.o_part + pidx * kHD;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t u[32];
+          tmem_ld_x32(tmem_o + lane_off + 32 * c, u);
+          tmem_ld_wait();
+          if (row_ok) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+              *reinterpret_cast<float4*>(o + 32 * c + i) =
+                  make_float4(__uint_as_float(u[i]) * inv, __uint_as_float(u[i + 1]) * inv,
+                              __uint_as_float(u[i + 2]) * inv, __uint_as_float(u[i + 3]) * inv);
+          }
+        }
+        if (row_ok) a.lse_part[pidx] = m_run + log2f(l_run);
+      }
+    }
+  done:;
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, kTmemColsTC);
+  }
+}
+
 // P enters the PV MMA as bf16 (the FlashAttention convention); CORTEX_FMHA_PLO=1 adds the
 // lo half (P = hi + lo to ~2^-17, a second PV pass). Measured on config 1 against the fp32
 // oracle: worst call 6.0e-4 / position 1.52e-3 (bf16 P) vs 5.1e-4 / 1.46e-3 (hi + lo); the
@@ -568,14 +929,52 @@ int fmha_p_lo() {
   return v;
 }
 
+// Kernel choice per launch (g_fmha_2q: -1 automatic, 0 one Q tile, 1 two; test / A-B
+// hook cortex_fmha_set_2q, env CORTEX_FMHA_2Q=0/1). A two-tile CTA costs ~1.55x a one-tile
+// CTA (benchmarks/fmha.py: 8K causal prefill 614 -> 807 TFLOP/s, 8 x 200-token prompts
+// 325 -> 406) but the grid halves, so small grids (decode's cascade pass over a
+// 1000-token prefix: 128 one-tile CTAs, 15 us vs 21 us) stay on one tile per CTA:
+// pick the lower of waves(n1) and 1.55 waves(n1 / 2) on the SM count.
+int g_fmha_2q = -2;
+int g_fmha_sms = 0;
+
+bool fmha_use_2q(const dim3& grid) {
+  if (g_fmha_2q == -2) {
+    const char* e = getenv("CORTEX_FMHA_2Q");
+    g_fmha_2q = (e && (e[0] == '0' || e[0] == '1')) ? e[0] - '0' : -1;
+  }
+  if (g_fmha_2q >= 0) return g_fmha_2q == 1;
+  if (g_fmha_sms == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&g_fmha_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      g_fmha_sms = 148;
+  }
+  const long yz = static_cast<long>(grid.y) * grid.z;
+  const long n1 = grid.x * yz, n2 = ((grid.x + 1) / 2) * yz;
+  const double w1 = static_cast<double>((n1 + g_fmha_sms - 1) / g_fmha_sms);
+  const double w2 = 1.55 * static_cast<double>((n2 + g_fmha_sms - 1) / g_fmha_sms);
+  return w2 < w1;
+}
+
+// grid.x counts query tiles of tpb tokens; the two-tile kernel takes them in pairs
 int32_t launch_fmha(const CUtensorMap* tq, const CUtensorMap* tkv, const FmhaArgs& a, dim3 grid,
                     cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(fmha_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kSmemTC) != cudaSuccess)
+                             kSmemTC) != cudaSuccess ||
+        cudaFuncSetAttribute(fmha2_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSmemTC2) != cudaSuccess)
       return CORTEX_ECUDA;
     configured = true;
+  }
+  if (!a.p_lo && fmha_use_2q(grid)) {
+    dim3 g2((grid.x + 1) / 2, grid.y, grid.z);
+    if (pdl_launch(fmha2_tc_kernel, g2, kThreadsTC, kSmemTC2, stream, 1, *tq, *tkv, a) !=
+        cudaSuccess)
+      return CORTEX_ECUDA;
+    return CORTEX_OK;
   }
   if (pdl_launch(fmha_tc_kernel, grid, kThreadsTC, kSmemTC, stream, 1, *tq, *tkv, a) != cudaSuccess)
     return CORTEX_ECUDA;
@@ -585,6 +984,13 @@ int32_t launch_fmha(const CUtensorMap* tq, const CUtensorMap* tkv, const FmhaArg
 }  // namespace
 
 extern "C" {
+
+// -1: choose per launch (default), 1: two Q tiles per CTA, 0: one (test / A-B hook)
+int32_t cortex_fmha_set_2q(int32_t on) {
+  if (on < -1 || on > 1) return CORTEX_EBADARG;
+  g_fmha_2q = on;
+  return CORTEX_OK;
+}
 
 int32_t cortex_fmha_prefill_tc(const void* tmap_kv, const void* tmap_q, void* out,
                                const int32_t* table, int32_t table_stride, const int32_t* seq_row,

@@ -111,6 +111,12 @@ def gemm_set_mode(mode: int) -> None:
     _check(lib().cortex_gemm_set_mode(mode), "cortex_gemm_set_mode")
 
 
+def fmha_set_2q(on: int) -> None:
+    """-1: per-launch choice (default), 1: two Q tiles per CTA in the tcgen05 attention,
+    0: one."""
+    _check(lib().cortex_fmha_set_2q(on), "cortex_fmha_set_2q")
+
+
 def gemm_set_stream_k(force: int) -> None:
     """-1 automatic, 0 whole tiles, 1 stream-K (2-SM kernel scheduling)."""
     _check(lib().cortex_gemm_set_stream_k(force), "cortex_gemm_set_stream_k")

@@ -334,7 +334,7 @@ def test_paged_decode_attention(cuda, group, flat):
 
 @pytest.mark.parametrize("group", [4, 2])
 @pytest.mark.parametrize("plens", [(1000, 40), (8192,), (16, 5, 0)])
-@pytest.mark.parametrize("impl", ["mma", "tc", "tc-flat"])
+@pytest.mark.parametrize("impl", ["mma", "tc", "tc1", "tc-flat"])
 def test_cascade_decode_attention(cuda, group, plens, impl):
     """Shared-prefix decode: calls grouped by resident prefix, prefix attended once."""
     o = ops()
@@ -388,10 +388,14 @@ def test_cascade_decode_attention(cuda, group, plens, impl):
     ga = np.asarray(grp, dtype=np.int32).reshape(-1, 4).T
     groups = (dev(ga[0]), dev(ga[1]), dev(ga[2]), dev(ga[3]), len(grp), int(ga[3].max()), pslots)
     k0, v0 = _rows(0, nb, hkv)
-    o.paged_decode_attn(o.kv_map(cache.view(-1, 128)), q, table, dev(seq_row), dev(seq_pre),
-                        dev(seq_kv), B, hkv, group, k0, v0, 1 / math.sqrt(128), o_part, lse_part,
-                        max_splits, out, groups=groups,
-                        qmap=o.QMap(q, hq, group) if impl != "mma" else None, flat=plan)
+    o.fmha_set_2q(0 if impl == "tc1" else 1)
+    try:
+        o.paged_decode_attn(o.kv_map(cache.view(-1, 128)), q, table, dev(seq_row), dev(seq_pre),
+                            dev(seq_kv), B, hkv, group, k0, v0, 1 / math.sqrt(128), o_part,
+                            lse_part, max_splits, out, groups=groups,
+                            qmap=o.QMap(q, hq, group) if impl != "mma" else None, flat=plan)
+    finally:
+        o.fmha_set_2q(-1)
     torch.cuda.synchronize()
     for b in range(B):
         k, v = _logical_kv(cache, 0, table[seq_row[b]].cpu(), seq_pre[b], seq_kv[b])
@@ -401,15 +405,16 @@ def test_cascade_decode_attention(cuda, group, plens, impl):
 
 
 @pytest.mark.parametrize("group", [4, 2])
-@pytest.mark.parametrize("impl", ["mma", "tc"])
+@pytest.mark.parametrize("impl", ["mma", "tc", "tc1"])
 def test_paged_prefill_attention(cuda, group, impl):
+    """tc: two-Q-tile tcgen05 kernel (default), tc1: one tile per CTA, mma: mma.sync."""
     o = ops()
     hkv, L, nb, max_blocks = 2, 1, 512, 160
     hq = hkv * group
     cache = _make_cache(cuda, L, nb, hkv, seed=23 + group)
     rng = np.random.default_rng(9)
     specs, tables = _seq_specs(rng, nb, max_blocks)
-    qlens = [min(kv, q) for (p, kv), q in zip(specs, [1, 17, 1, 37, 137, 100, 256, 255, 3, 257, 700])]
+    qlens = [min(kv, q) for (p, kv), q in zip(specs, [1, 17, 1, 37, 137, 100, 256, 255, 3, 257, 700, 300, 65, 200])]
     B = len(specs)
     table = torch.zeros(B, max_blocks, dtype=torch.int32)
     for i, t in enumerate(tables):
@@ -427,7 +432,11 @@ def test_paged_prefill_attention(cuda, group, impl):
     if impl == "mma":
         o.paged_prefill_attn(kvmap, q, out, *args)
     else:
-        o.fmha_prefill(kvmap, o.QMap(q, hq, group), out, *args)
+        o.fmha_set_2q(0 if impl == "tc1" else 1)
+        try:
+            o.fmha_prefill(kvmap, o.QMap(q, hq, group), out, *args)
+        finally:
+            o.fmha_set_2q(-1)
     torch.cuda.synchronize()
     for b, (prefix, kvlen) in enumerate(specs):
         k, v = _logical_kv(cache, 0, table[b].cpu(), prefix, kvlen)
