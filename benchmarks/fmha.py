@@ -73,7 +73,7 @@ def prefill(prefix: int, prompts: list[int]) -> dict:
             "ms": ms, "tflops": flops / ms / 1e9, "mma_sync_ms": ms_mma}
 
 
-def cascade(prefix: int, n_calls: int, groups: int = 2) -> dict:
+def cascade(prefix: int, n_calls: int, groups: int = 2, pslots: int | None = None) -> dict:
     dev = torch.device("cuda")
     npb = (prefix + 15) // 16
     nb = groups * npb + 16
@@ -84,7 +84,7 @@ def cascade(prefix: int, n_calls: int, groups: int = 2) -> dict:
     table = table.to(dev)
     B = groups * n_calls
     q = torch.randn(B, HQ, 128, device=dev).to(torch.bfloat16)
-    pslots = (npb + 15) // 16
+    pslots = pslots or (npb + 15) // 16
     o_part = torch.empty(B * (pslots + 1) * HQ * 128, device=dev)
     lse = torch.empty(B * (pslots + 1) * HQ, device=dev)
     d = lambda a: torch.as_tensor(np.asarray(a, np.int32), device=dev)
@@ -103,7 +103,7 @@ def cascade(prefix: int, n_calls: int, groups: int = 2) -> dict:
 
     ms = _time(run)
     flops = 4.0 * B * HQ * prefix * 128
-    return {"kind": "cascade", "prefix": prefix, "calls": B, "ms": ms,
+    return {"kind": "cascade", "prefix": prefix, "calls": B, "slots": pslots, "ms": ms,
             "tflops": flops / ms / 1e9}
 
 
@@ -116,3 +116,12 @@ if __name__ == "__main__":
             r["q_tiles_per_cta"] = {1: 2, 0: 1, -1: "auto"}[q2]
             print(json.dumps(r), flush=True)
     ops.fmha_set_2q(-1)
+    if "--slots" in sys.argv:  # the bench's cascade shapes: prefix slots x kernel
+        for prefix, n in ((1000, 108), (8192, 128)):
+            for sl in (1, 2, 3, 4, 6, 8):
+                for q2 in (0, 1):
+                    ops.fmha_set_2q(q2)
+                    r = cascade(prefix, n, pslots=sl)
+                    r["q_tiles_per_cta"] = 2 if q2 else 1
+                    print(json.dumps(r), flush=True)
+        ops.fmha_set_2q(-1)

@@ -235,7 +235,8 @@ class GpuWorker:
         self.tc_attention = os.environ.get("CORTEX_TC_ATTN", "1") != "0"
         self.qmap = ops.QMap(self.q, cfg.n_heads, cfg.group)
         self.overlap_cascade = True
-        self.cascade_slots = int(os.environ.get("CORTEX_CASCADE_SLOTS", "2"))
+        # prefix slots of the cascade pass: 0 = by prefix length (below), or a fixed count
+        self.cascade_slots = int(os.environ.get("CORTEX_CASCADE_SLOTS", "0"))
         # balanced decode plan (equal tile ranges per CTA) instead of per-call 512-token
         # splits; measured slower on config-2 contexts (benchmarks/attn_step.py), so opt-in
         self.flat_decode = os.environ.get("CORTEX_FLAT_DECODE", "0") == "1"
@@ -418,9 +419,13 @@ class GpuWorker:
         garr = np.asarray(groups, i32).reshape(-1, 4).T.copy() if groups else np.zeros((4, 0), i32)
         pslots = 0
         if n_dec and groups:
-            # prefix partial slots (each a run of key tiles of the cascade pass)
-            pslots = min(self.cascade_slots,
-                         int(((garr[1] + BLOCK_TOKENS - 1) // BLOCK_TOKENS + 15).max() // 16))
+            # prefix partial slots (each a run of key tiles of the cascade pass): 2 up to
+            # 2K-token prefixes, 4 beyond (benchmarks/fmha.py --slots, per layer: P = 1000
+            # 2 slots 15.7 us (1 slot 22.0, 4 slots 17.8); P = 8192 4 slots 52.2 us with two
+            # Q tiles per CTA (2 slots 64.7, 8 slots 60.6))
+            npb_max = int(((garr[1] + BLOCK_TOKENS - 1) // BLOCK_TOKENS).max())
+            want = self.cascade_slots or min(4, max(2, -(-npb_max // 128)))
+            pslots = min(want, (npb_max + 15) // 16)
         fplan = None
         if n_dec and self.flat_decode:
             fplan = ops.decode_flat_plan(dec_prefix, dec_kvlen, cfg.n_kv_heads, bool(groups),
