@@ -215,6 +215,39 @@ CORTEX_DEVICE float ex2_approx(float x) {  // 2^x, one MUFU op (-inf -> 0)
   return y;
 }
 
+// Max / sum of 64 values through 8 independent accumulators: a single running
+// accumulator is a 64-deep dependent chain (~4 cycles per link) that one softmax warp per
+// SM sub-partition cannot hide.
+CORTEX_DEVICE float max64(const float (&v)[64], float init) {
+  float m[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) m[k] = v[k];
+#pragma unroll
+  for (int i = 8; i < 64; i += 8)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m[k] = fmaxf(m[k], v[i + k]);
+#pragma unroll
+  for (int w = 4; w > 0; w >>= 1)
+#pragma unroll
+    for (int k = 0; k < w; ++k) m[k] = fmaxf(m[k], m[k + w]);
+  return fmaxf(init, m[0]);
+}
+
+CORTEX_DEVICE float sum64(const float (&v)[64]) {
+  float t[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) t[k] = v[k];
+#pragma unroll
+  for (int i = 8; i < 64; i += 8)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t[k] += v[i + k];
+#pragma unroll
+  for (int w = 4; w > 0; w >>= 1)
+#pragma unroll
+    for (int k = 0; k < w; ++k) t[k] += t[k + w];
+  return t[0];
+}
+
 __global__ void __launch_bounds__(kThreadsTC, 1)
     fmha_tc_kernel(const __grid_constant__ CUtensorMap tmap_q,
                    const __grid_constant__ CUtensorMap tmap_kv, const FmhaArgs a) {
@@ -407,13 +440,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       mbar_wait_guard(&s_full[s], (kt / kStagesTC) & 1);
       tc_fence_after();
       float sv[64];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t u[32];
-        tmem_ld_x32(tmem_s + 128 * s + lane_off + 64 * half + 32 * c, u);
+      {
+        uint32_t u0[32], u1[32];  // both loads in flight, one wait
+        tmem_ld_x32(tmem_s + 128 * s + lane_off + 64 * half, u0);
+        tmem_ld_x32(tmem_s + 128 * s + lane_off + 64 * half + 32, u1);
         tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) sv[32 * c + i] = __uint_as_float(u[i]);
+        for (int i = 0; i < 32; ++i) {
+          sv[i] = __uint_as_float(u0[i]);
+          sv[32 + i] = __uint_as_float(u1[i]);
+        }
       }
       // tile max (raw scores; scale > 0 commutes with max). Fast path when every key
       // of the tile is valid and visible to every row of the CTA (CTA-uniform test);
@@ -425,11 +461,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const BlockSpan b = block_span(prefix_len, kv_len, j0 + j, blk_end);
         full = full && b.nvalid == kBlk && b.pos0 + kBlk - 1 <= qpos_base;
       }
-      float mraw = -INFINITY;
-      if (full) {
-#pragma unroll
-        for (int i = 0; i < 64; ++i) mraw = fmaxf(mraw, sv[i]);
-      } else {
+      if (!full) {
 #pragma unroll
         for (int j = 0; j < kBlocksPerTile / 2; ++j) {
           const BlockSpan b = block_span(prefix_len, kv_len, j0 + 4 * half + j, blk_end);
@@ -437,10 +469,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           for (int i = 0; i < kBlk; ++i) {
             const bool ok = row_ok && i < b.nvalid && b.pos0 + i <= qpos;
             sv[kBlk * j + i] = ok ? sv[kBlk * j + i] : -INFINITY;
-            mraw = fmaxf(mraw, sv[kBlk * j + i]);
           }
         }
       }
+      float mraw = max64(sv, -INFINITY);
       xmax[((kt & 1) * 2 + half) * kRows + r] = mraw;
       named_bar_sync(bar_id, 64);
       mraw = fmaxf(mraw, xmax[((kt & 1) * 2 + (half ^ 1)) * kRows + r]);
@@ -453,12 +485,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       const float m_new = adopt ? mt : m_run;
       const float m_use = m_new == -INFINITY ? 0.f : m_new;
       // p = exp2(s * scale - m), computed before waiting for the previous PV
-      float lsum = 0.f;
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        sv[i] = ex2_approx(fmaf(sv[i], a.scale_log2, -m_use));
-        lsum += sv[i];
-      }
+      for (int i = 0; i < 64; ++i) sv[i] = ex2_approx(fmaf(sv[i], a.scale_log2, -m_use));
+      const float lsum = sum64(sv);
       // O rescale of this half's 64 dims (rare; tcgen05.ld/st are warp-collective:
       // decided per warp - the partner warp sees the same rows - alpha per row) needs
       // PV of the previous tile finished
@@ -798,24 +827,23 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           }
         };
         auto load_half = [&](float (&v)[64], int h) {
+          uint32_t u0[32], u1[32];  // both loads in flight, one wait
+          tmem_ld_x32(tmem_s + lane_off + 64 * h, u0);
+          tmem_ld_x32(tmem_s + lane_off + 64 * h + 32, u1);
+          tmem_ld_wait();
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            uint32_t u[32];
-            tmem_ld_x32(tmem_s + lane_off + 64 * h + 32 * c, u);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[32 * c + i] = __uint_as_float(u[i]);
+          for (int i = 0; i < 32; ++i) {
+            v[i] = __uint_as_float(u0[i]);
+            v[32 + i] = __uint_as_float(u1[i]);
           }
           if (!full) mask_half(v, h);
         };
         float sv[64];
         float mraw = -INFINITY;
         load_half(sv, 1);
-#pragma unroll
-        for (int i = 0; i < 64; ++i) mraw = fmaxf(mraw, sv[i]);
+        mraw = max64(sv, mraw);
         load_half(sv, 0);
-#pragma unroll
-        for (int i = 0; i < 64; ++i) mraw = fmaxf(mraw, sv[i]);
+        mraw = max64(sv, mraw);
         const float mt = mraw * a.scale_log2;
         const bool adopt = mt > -INFINITY && (m_run == -INFINITY || mt > m_run + kRescaleThresh);
         const float alpha = !adopt ? 1.f : (m_run == -INFINITY ? 0.f : exp2f(m_run - mt));
@@ -844,10 +872,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         for (int h = 0; h < 2; ++h) {
           if (h == 1) load_half(sv, 1);
 #pragma unroll
-          for (int i = 0; i < 64; ++i) {
-            sv[i] = ex2_approx(fmaf(sv[i], a.scale_log2, -m_use));
-            lsum += sv[i];
-          }
+          for (int i = 0; i < 64; ++i) sv[i] = ex2_approx(fmaf(sv[i], a.scale_log2, -m_use));
+          lsum += sum64(sv);
           uint32_t hi[32];
 #pragma unroll
           for (int c = 0; c < 32; ++c) hi[c] = pack_bf16(sv[2 * c], sv[2 * c + 1]);
