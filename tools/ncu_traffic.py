@@ -18,8 +18,9 @@ import sys
 
 CLASSES = {
     "gemm": ("gemm_bf16",),
-    "attn_decode": ("paged_decode", "cascade_prefix", "decode_combine", "fmha_tc_kernel"),
-    "attn_prefill": ("fmha_tc_kernel", "paged_prefill"),
+    "attn_decode": ("paged_decode", "cascade_prefix", "decode_combine", "fmha_tc_kernel",
+                    "fmha2_tc_kernel"),
+    "attn_prefill": ("fmha_tc_kernel", "fmha2_tc_kernel", "paged_prefill"),
 }
 
 
