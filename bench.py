@@ -300,7 +300,9 @@ def main() -> None:
         coll_barrier()
 
     # kernel-class shares (untimed) -> the dominant kernel for the roofline
-    w.prof = KernelProfile(["gemm", "attn_decode", "attn_prefill"])
+    # attn_decode_ctx (the per-call context splits alone, nested in attn_decode) is the
+    # HBM-bound decode-attention kernel the north star's >= 70 % target is about
+    w.prof = KernelProfile(["gemm", "attn_decode", "attn_prefill", "attn_decode_ctx"])
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -309,7 +311,8 @@ def main() -> None:
     shares = w.prof.summary()
     prof_ms = e0.elapsed_time(e1)
     w.prof = None
-    dominant = max(shares, key=lambda k: shares[k]["ms"]) if shares else "gemm"
+    dominant = max((k for k in shares if k != "attn_decode_ctx"),
+                   key=lambda k: shares[k]["ms"], default="gemm")
 
     # ---------------- timed region ----------------
     peaks, peak_src = _peaks()

@@ -474,6 +474,10 @@ class GpuWorker:
             uniq += sum({(d.prefix_key if d.prefix_key >= 0 else ("row", d.row)): d.prefix_len
                          for d in plan.decode}.values())
             dec_bytes = uniq * tok_kv_bytes + n_dec * hq * HEAD_DIM * 2 * 2
+            # the per-call context splits alone (private KV, HBM-bound kernel)
+            ctx_bytes = (sum(d.kv_len - d.prefix_len for d in plan.decode) * tok_kv_bytes
+                         + n_dec * hq * HEAD_DIM * 2 * 2)
+            ctx_flops = 4.0 * hq * HEAD_DIM * sum(d.kv_len - d.prefix_len for d in plan.decode)
             dec_flops = 4.0 * hq * HEAD_DIM * float(dec_kvlen.sum())
             pf_keys = sum(int(q) * (int(k) - int(q)) + int(q) * (int(q) + 1) // 2
                           for q, k in zip(pf_qlen, pf_kvlen))
@@ -525,14 +529,21 @@ class GpuWorker:
                     main = torch.cuda.current_stream()
                     self._ev_fork.record(main)
                     self.side.wait_event(self._ev_fork)
+
+                    def ctx_splits():
+                        e2 = prof.open("attn_decode_ctx") if prof is not None else None
+                        ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=2,
+                                              flat=flat)
+                        if e2 is not None:
+                            prof.close("attn_decode_ctx", e2, ctx_bytes, ctx_flops)
+
                     ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=1,
                                           stream=self.side)
                     if n_pf:
                         prefill_attn(self.side)
                         pf_done = True
                         nl += 1
-                    ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=2,
-                                          flat=flat)
+                    ctx_splits()
                     self._ev_join.record(self.side)
                     main.wait_event(self._ev_join)
                     ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=4,

@@ -21,6 +21,7 @@ CLASSES = {
     "attn_decode": ("paged_decode", "cascade_prefix", "decode_combine", "fmha_tc_kernel",
                     "fmha2_tc_kernel"),
     "attn_prefill": ("fmha_tc_kernel", "fmha2_tc_kernel", "paged_prefill"),
+    "attn_decode_ctx": ("paged_decode",),
 }
 
 
