@@ -588,10 +588,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 // Two-Q-tile variant (ping-pong): one CTA owns 2 x 128 query rows (Q tiles A and B,
 // 2 x tpb tokens) and streams every K/V tile once for both, so the L2 -> SM traffic per
 // flop halves, and the tensor pipe computes one tile's S / PV while the other tile's
-// softmax runs:
-//   MMA warp: S_A(0) S_B(0) | PV_A(t) S_A(t+1) PV_B(t) S_B(t+1) | ...
-//   softmax warpgroup A (warps 2-5) and B (warps 6-9): one thread per query row, all
-//   128 keys of the tile (no cross-warp max exchange), lazy O rescale, P -> TMEM.
+// softmax runs. The work unit is half a key tile (64 keys): S of one half is computed
+// while the same warpgroup's softmax works on the other half (S_X(t+1, h) is issued
+// right behind PV_X(t, h), which frees those TMEM columns):
+//   MMA warp: S(0,0) S(0,1) | per half h: PV_A(t,h) S_A(t+1,h) PV_B(t,h) S_B(t+1,h) | ...
+//   softmax warpgroup A (warps 2-5) and B (warps 6-9): one thread per query row, 64 keys
+//   per unit (no cross-warp max exchange), lazy O rescale, P -> TMEM.
 // TMEM: S_A [0,128)  S_B [128,256)  O_A [256,384)  O_B [384,512) (S single-buffered per
 // tile: S_X(t+1) is issued after PV_X(t), which consumed P_X(t) in place, in MMA order).
 // Smem: Q_A 32 KiB, Q_B 32 KiB, 2 K/V stages of 64 KiB, barriers.
@@ -614,11 +616,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   uint64_t* k_empty = bars + 3;  // [2]
   uint64_t* v_full = bars + 5;   // [2]
   uint64_t* v_empty = bars + 7;  // [2]
-  uint64_t* s_full = bars + 9;   // [2 tiles]
-  uint64_t* p_full = bars + 11;  // [2 tiles]
-  uint64_t* o_ready = bars + 13; // [2 tiles] committed after every PV of the tile
-  uint64_t* o_done = bars + 15;  // [2 tiles]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 17);
+  uint64_t* s_full = bars + 9;   // [2 tiles][2 key halves]
+  uint64_t* p_full = bars + 13;  // [2 tiles][2 key halves]
+  uint64_t* o_ready = bars + 17; // [2 tiles] committed after every PV of the tile
+  uint64_t* o_done = bars + 19;  // [2 tiles]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 21);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -675,9 +677,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
     }
-    for (int x = 0; x < 2; ++x) {
+    for (int x = 0; x < 4; ++x) {
       mbar_init(&s_full[x], 1);
       mbar_init(&p_full[x], 4);
+    }
+    for (int x = 0; x < 2; ++x) {
       mbar_init(&o_ready[x], 1);
       mbar_init(&o_done[x], 1);
     }
@@ -729,40 +733,43 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     }
   } else if (warp == 1) {
     if (elect_one()) {
-      // ---- MMA issuer ----
-      constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128);
+      // ---- MMA issuer: work unit = (key tile, 64-key half), so S of one half computes
+      // while the same warpgroup's softmax runs on the other half ----
+      constexpr uint32_t idesc_s = umma_idesc_bf16(128, 64);                 // N = 64 keys
       constexpr uint32_t idesc_pv = umma_idesc_bf16(128, 128) | (1u << 16);  // V MN-major
       const int nx = has_b ? 2 : 1;
       mbar_wait_guard(q_full, 0);
-      auto issue_s = [&](int kt, int x) {
+      auto issue_s = [&](int kt, int x, int h) {  // S_x(kt, h) -> TMEM S_x cols [64h, +64)
         const int s = kt % kStagesTC;
         const uint32_t q_addr = smem_u32(smem + kOffQ2 + x * kQBytes);
-        const uint32_t k_addr = smem_u32(smem + kOffKV2 + s * kKVStage);
+        const uint32_t k_addr = smem_u32(smem + kOffKV2 + s * kKVStage) + h * 64 * 128;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t off = (kk >> 2) * kKVHalf + (kk & 3) * 32;
-          umma_bf16_ss(tmem + 128 * x, umma_desc_sw128(q_addr + off),
+          umma_bf16_ss(tmem + 128 * x + 64 * h, umma_desc_sw128(q_addr + off),
                        umma_desc_sw128(k_addr + off), idesc_s, kk != 0 ? 1u : 0u);
         }
-        umma_commit(&s_full[x]);
+        umma_commit(&s_full[2 * x + h]);
       };
-      auto issue_pv = [&](int kt, int x) {
+      auto issue_pv = [&](int kt, int x, int h) {  // O_x += P_x(kt, h) V(kt, keys of h)
         const int s = kt % kStagesTC;
         const uint32_t v_addr = smem_u32(smem + kOffKV2 + s * kKVStage + 2 * kKVHalf);
-        const uint32_t p_tmem = tmem + 128 * x;
+        const uint32_t p_tmem = tmem + 128 * x + 64 * h;
         const uint32_t o_tmem = tmem + 256 + 128 * x;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          umma_bf16_ts(o_tmem, p_tmem + 8 * kk, umma_desc_sw128_mn(v_addr + kk * 2048, kKVHalf),
-                       idesc_pv, (kt | kk) != 0 ? 1u : 0u);
+        for (int kk = 0; kk < 4; ++kk) {
+          umma_bf16_ts(o_tmem, p_tmem + 8 * kk,
+                       umma_desc_sw128_mn(v_addr + (4 * h + kk) * 2048, kKVHalf), idesc_pv,
+                       (kt | h | kk) != 0 ? 1u : 0u);
         }
         umma_commit(&o_ready[x]);
-        if (kt == n_kt - 1) umma_commit(&o_done[x]);
+        if (kt == n_kt - 1 && h == 1) umma_commit(&o_done[x]);
       };
       if (n_kt > 0) {
         mbar_wait_guard(&k_full[0], 0);
         tc_fence_after();
-        for (int x = 0; x < nx; ++x) issue_s(0, x);
+        for (int h = 0; h < 2; ++h)
+          for (int x = 0; x < nx; ++x) issue_s(0, x, h);
         umma_commit(&k_empty[0]);
       }
       for (int kt = 0; kt < n_kt; ++kt) {
@@ -770,16 +777,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const bool more = kt + 1 < n_kt;
         const int s1 = (kt + 1) % kStagesTC;
         mbar_wait_guard(&v_full[s], (kt / kStagesTC) & 1);
-        for (int x = 0; x < nx; ++x) {
-          mbar_wait_guard(&p_full[x], kt & 1);
-          tc_fence_after();
-          issue_pv(kt, x);
-          if (more) {  // S_x(kt+1) right behind PV_x(kt), while the other tile's softmax runs
-            if (x == 0) {
-              mbar_wait_guard(&k_full[s1], ((kt + 1) / kStagesTC) & 1);
-              tc_fence_after();
+        for (int h = 0; h < 2; ++h) {
+          for (int x = 0; x < nx; ++x) {
+            mbar_wait_guard(&p_full[2 * x + h], kt & 1);
+            tc_fence_after();
+            issue_pv(kt, x, h);
+            if (more) {  // S_x(kt+1, h) into the half PV_x(kt, h) just released
+              if (h == 0 && x == 0) {
+                mbar_wait_guard(&k_full[s1], ((kt + 1) / kStagesTC) & 1);
+                tc_fence_after();
+              }
+              issue_s(kt + 1, x, h);
             }
-            issue_s(kt + 1, x);
           }
         }
         umma_commit(&v_empty[s]);
@@ -801,90 +810,78 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       const int qpos0 = qpos_base == 0x3fffffff ? qpos_base : qpos_base + x * tpb;
       const int qpos = qpos0 == 0x3fffffff ? qpos0 : qpos0 + r / group;
       float m_run = -INFINITY, l_run = 0.f;
-      for (int kt = 0; kt < n_kt; ++kt) {
-        mbar_wait_guard(&s_full[x], kt & 1);
+      for (int u = 0; u < 2 * n_kt; ++u) {
+        const int kt = u >> 1, h = u & 1;
+        mbar_wait_guard(&s_full[2 * x + h], kt & 1);
         tc_fence_after();
-        // keys [0, 64) stay in registers; keys [64, 128) are read twice from TMEM (max,
-        // then exp) to keep the thread at 64 live scores (168-register budget)
-        const int j0 = blk_begin + kt * kBlocksPerTile;
-        // fast path (tile-uniform): every key valid and visible to every row of the tile
-        bool full = j0 + kBlocksPerTile <= blk_end;
-#pragma unroll
-        for (int j = 0; j < kBlocksPerTile; ++j) {
-          const BlockSpan b = block_span(prefix_len, kv_len, j0 + j, blk_end);
-          full = full && b.nvalid == kBlk && b.pos0 + kBlk - 1 <= qpos0;
-        }
-        // masks the 64 scores of key half h in place (invalid / causal / padding rows)
-        auto mask_half = [&](float (&v)[64], int h) {
-#pragma unroll
-          for (int j = 0; j < kBlocksPerTile / 2; ++j) {
-            const BlockSpan b = block_span(prefix_len, kv_len, j0 + 4 * h + j, blk_end);
-#pragma unroll
-            for (int i = 0; i < kBlk; ++i) {
-              const bool ok = row_ok && i < b.nvalid && b.pos0 + i <= qpos;
-              v[kBlk * j + i] = ok ? v[kBlk * j + i] : -INFINITY;
-            }
-          }
-        };
-        auto load_half = [&](float (&v)[64], int h) {
+        float sv[64];
+        {
           uint32_t u0[32], u1[32];  // both loads in flight, one wait
           tmem_ld_x32(tmem_s + lane_off + 64 * h, u0);
           tmem_ld_x32(tmem_s + lane_off + 64 * h + 32, u1);
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
-            v[i] = __uint_as_float(u0[i]);
-            v[32 + i] = __uint_as_float(u1[i]);
+            sv[i] = __uint_as_float(u0[i]);
+            sv[32 + i] = __uint_as_float(u1[i]);
           }
-          if (!full) mask_half(v, h);
-        };
-        float sv[64];
-        float mraw = -INFINITY;
-        load_half(sv, 1);
-        mraw = max64(sv, mraw);
-        load_half(sv, 0);
-        mraw = max64(sv, mraw);
-        const float mt = mraw * a.scale_log2;
+        }
+        // fast path (unit-uniform): every key valid and visible to every row of the tile;
+        // otherwise mask (invalid slots of partial blocks, causal, rows past the end)
+        const int jb = blk_begin + kt * kBlocksPerTile + 4 * h;
+        bool full = jb + 4 <= blk_end;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const BlockSpan b = block_span(prefix_len, kv_len, jb + j, blk_end);
+          full = full && b.nvalid == kBlk && b.pos0 + kBlk - 1 <= qpos0;
+        }
+        if (!full) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const BlockSpan b = block_span(prefix_len, kv_len, jb + j, blk_end);
+#pragma unroll
+            for (int i = 0; i < kBlk; ++i) {
+              const bool ok = row_ok && i < b.nvalid && b.pos0 + i <= qpos;
+              sv[kBlk * j + i] = ok ? sv[kBlk * j + i] : -INFINITY;
+            }
+          }
+        }
+        const float mt = max64(sv, -INFINITY) * a.scale_log2;
         const bool adopt = mt > -INFINITY && (m_run == -INFINITY || mt > m_run + kRescaleThresh);
         const float alpha = !adopt ? 1.f : (m_run == -INFINITY ? 0.f : exp2f(m_run - mt));
         const float m_new = adopt ? mt : m_run;
         const float m_use = m_new == -INFINITY ? 0.f : m_new;
-        if (kt > 0 && __any_sync(0xffffffffu, adopt && m_run != -INFINITY)) {
-          mbar_wait_guard(&o_ready[x], (kt - 1) & 1);
+        // O rescale (rare) needs the previous unit's PV done; PV of unit u-2 completed
+        // before S of this unit (same half, MMA order), so the parity wait is exact
+        if (u > 0 && __any_sync(0xffffffffu, adopt && m_run != -INFINITY)) {
+          mbar_wait_guard(&o_ready[x], (u - 1) & 1);
           tc_fence_after();
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            uint32_t u[32];
-            tmem_ld_x32(tmem_o + lane_off + 32 * c, u);
+            uint32_t uo[32];
+            tmem_ld_x32(tmem_o + lane_off + 32 * c, uo);
             tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * alpha);
-            tmem_st_x32(tmem_o + lane_off + 32 * c, u);
+            for (int i = 0; i < 32; ++i) uo[i] = __float_as_uint(__uint_as_float(uo[i]) * alpha);
+            tmem_st_x32(tmem_o + lane_off + 32 * c, uo);
           }
           tmem_st_wait();
         }
-        // p = exp2(s * scale - m); P as bf16 (keys 2c / 2c+1 packed in column c) over S
-        // columns [0, 64): half 0's P lands on S columns already consumed, half 1's
-        // scores (S columns [64, 128)) are re-read before any P column reaches them.
-        // (P hi + lo is the one-tile kernel's option.)
-        float lsum = 0.f;
+        // p = exp2(s * scale - m); P as bf16 (keys 2c / 2c+1 packed in column c) over the
+        // first 32 columns of this half's S
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (h == 1) load_half(sv, 1);
+        for (int i = 0; i < 64; ++i) sv[i] = ex2_approx(fmaf(sv[i], a.scale_log2, -m_use));
+        const float lsum = sum64(sv);
+        uint32_t hi[32];
 #pragma unroll
-          for (int i = 0; i < 64; ++i) sv[i] = ex2_approx(fmaf(sv[i], a.scale_log2, -m_use));
-          lsum += sum64(sv);
-          uint32_t hi[32];
-#pragma unroll
-          for (int c = 0; c < 32; ++c) hi[c] = pack_bf16(sv[2 * c], sv[2 * c + 1]);
-          tmem_st_x32(tmem_s + lane_off + 32 * h, hi);
-        }
+        for (int c = 0; c < 32; ++c) hi[c] = pack_bf16(sv[2 * c], sv[2 * c + 1]);
+        tmem_st_x32(tmem_s + lane_off + 64 * h, hi);
         l_run = l_run * alpha + lsum;
         m_run = m_new;
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[x]);
+        if (lane == 0) mbar_arrive(&p_full[2 * x + h]);
       }
       // ---- epilogue: this tile's O rows ----
       mbar_wait_guard(&o_done[x], 0);
