@@ -38,7 +38,10 @@ constexpr float kRescaleThresh = 8.0f;  // log2 units
 constexpr int kQBytes = kRows * kHD * 2;                 // 32 KiB
 constexpr int kKVHalf = kBlocksPerTile * kBlk * 64 * 2;  // 16 KiB  [128 keys x 64 dims]
 constexpr int kKVStage = 4 * kKVHalf;                    // K lo, K hi, V lo, V hi
-constexpr int kStagesTC = 2;
+#ifndef CORTEX_FMHA_STAGES  // (overridable for tuning builds)
+#define CORTEX_FMHA_STAGES 2
+#endif
+constexpr int kStagesTC = CORTEX_FMHA_STAGES;
 constexpr int kOffQ = 0;
 constexpr int kOffKV = kQBytes;
 constexpr int kOffBar = kOffKV + kStagesTC * kKVStage;
