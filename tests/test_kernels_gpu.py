@@ -480,6 +480,15 @@ def test_rmsnorm_embed_swiglu_argmax(cuda):
     ref_tok = torch.argmax(logits, dim=1).to(torch.int32)
     assert torch.equal(tok, ref_tok)
     assert int(tok[3]) == 77
+    # ties inside one 16-byte load, across threads and in the scalar tail of an odd vocab
+    for vocab, ties in ((128256, (8, 9)), (128256, (4101, 5)), (1027, (1026, 1025)),
+                        (1027, (1024, 3))):
+        lg = torch.randn(2, vocab, generator=g, device=cuda)
+        lg[1, list(ties)] = 50.0
+        t2 = torch.empty(2, dtype=torch.int32, device=cuda)
+        o.argmax(lg, 2, vocab, out_tok=t2)
+        assert int(t2[1]) == min(ties), (vocab, ties)
+        assert int(t2[0]) == int(torch.argmax(lg[0]))
 
 
 def test_rope_kv_append(cuda):
