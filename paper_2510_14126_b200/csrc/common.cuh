@@ -19,6 +19,8 @@
 #define CORTEX_DEVICE __device__ __forceinline__
 
 #define CORTEX_BUILDING 1
+#include <cstdio>
+
 #include "cortex_b200.h"
 
 #define CORTEX_CHECK_LAUNCH()                      \
@@ -114,15 +116,32 @@ CORTEX_DEVICE void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 
-CORTEX_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t addr = smem_u32(bar);
+CORTEX_DEVICE bool mbar_try_wait(uint32_t addr, uint32_t parity) {
+  uint32_t done;
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(addr),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}\n"
+      : "=r"(done)
+      : "r"(addr), "r"(parity)
       : "memory");
+  return done != 0;
+}
+
+// mbarrier wait; a phase that never completes (~9 s of SM clock) traps with a diagnostic
+// (grid, block, thread, barrier, parity) instead of hanging the GPU.
+CORTEX_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  if (mbar_try_wait(addr, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try_wait(addr, parity)) {
+    if (clock64() - t0 > (16ll << 30)) {
+      printf("cortex mbar hang: grid (%d,%d,%d) block (%d,%d,%d) thread %d smem+%u parity %u\n",
+             gridDim.x, gridDim.y, gridDim.z, blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x,
+             addr & 0x3ffff, parity);
+      __trap();
+    }
+  }
 }
 
 // --------------------------------------------------------------------------

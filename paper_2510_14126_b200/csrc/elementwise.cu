@@ -196,8 +196,10 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int64_t ld, int 
   __shared__ int si[32];
   const int r = blockIdx.x;
   const float* row = logits + r * ld;
+  // NaN never compares greater, so a row of NaN logits yields index 0 (a valid token id
+  // for the embedding lookup of the next step) rather than an out-of-range sentinel
   float best = -INFINITY;
-  int bi = 0x7fffffff;
+  int bi = vocab;
   auto take = [&](float v, int i) {
     if (v > best) {  // strictly greater: keeps the first index within a thread
       best = v;
@@ -252,6 +254,7 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int64_t ld, int 
         bi = si[w];
       }
     }
+    if (bi >= vocab) bi = 0;  // no finite logit in the row
     if (out_tok) out_tok[r] = bi;
     if (slot) {
       const int s = slot[r];

@@ -489,6 +489,10 @@ def test_rmsnorm_embed_swiglu_argmax(cuda):
         o.argmax(lg, 2, vocab, out_tok=t2)
         assert int(t2[1]) == min(ties), (vocab, ties)
         assert int(t2[0]) == int(torch.argmax(lg[0]))
+    # a row without a finite logit still yields a valid token id (0)
+    lg = torch.full((1, 128256), float("nan"), device=cuda)
+    o.argmax(lg, 1, 128256, out_tok=t2)
+    assert int(t2[0]) == 0
 
 
 def test_rope_kv_append(cuda):
