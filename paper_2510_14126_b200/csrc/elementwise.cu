@@ -129,17 +129,25 @@ __global__ void rope_kv_append_kernel(const RopeArgs a) {
   const float* st = a.sin_tab + static_cast<int64_t>(pos) * 64;
   const int block = a.table[static_cast<int64_t>(a.tok_row[t]) * a.table_stride + a.tok_col[t]];
   const int off = a.tok_off[t];
-  // rotate q and k heads: (head, pair i) work items
-  const int n_rot = (a.hq + a.hkv) * 64;
+  // rotate q and k heads: work item = (head, 8 consecutive pairs (i, i + 64)), 16-byte
+  // loads and stores of both halves, cos / sin as float4
+  const int n_rot = (a.hq + a.hkv) * 8;
   for (int item = threadIdx.x; item < n_rot; item += blockDim.x) {
-    const int h = item / 64;
-    const int i = item % 64;
+    const int h = item >> 3;
+    const int i0 = (item & 7) * 8;
     const __nv_bfloat16* xh = src + h * kHeadDim;
-    const float x0 = __bfloat162float(xh[i]);
-    const float x1 = __bfloat162float(xh[i + 64]);
-    const float c = ct[i], s = st[i];
-    const float y0 = x0 * c - x1 * s;
-    const float y1 = x1 * c + x0 * s;
+    float x0[8], x1[8], c[8], sn[8], y0[8], y1[8];
+    unpack8(*reinterpret_cast<const bf16x8*>(xh + i0), x0);
+    unpack8(*reinterpret_cast<const bf16x8*>(xh + 64 + i0), x1);
+    *reinterpret_cast<float4*>(c) = *reinterpret_cast<const float4*>(ct + i0);
+    *reinterpret_cast<float4*>(c + 4) = *reinterpret_cast<const float4*>(ct + i0 + 4);
+    *reinterpret_cast<float4*>(sn) = *reinterpret_cast<const float4*>(st + i0);
+    *reinterpret_cast<float4*>(sn + 4) = *reinterpret_cast<const float4*>(st + i0 + 4);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      y0[e] = x0[e] * c[e] - x1[e] * sn[e];
+      y1[e] = x1[e] * c[e] + x0[e] * sn[e];
+    }
     __nv_bfloat16* dst;
     if (h < a.hq) {
       dst = a.q_out + (static_cast<int64_t>(t) * a.hq + h) * kHeadDim;
@@ -147,8 +155,8 @@ __global__ void rope_kv_append_kernel(const RopeArgs a) {
       const int kh = h - a.hq;
       dst = a.cache + (a.k_row0 + (static_cast<int64_t>(block) * a.hkv + kh) * kTile + off) * kHeadDim;
     }
-    dst[i] = __float2bfloat16_rn(y0);
-    dst[i + 64] = __float2bfloat16_rn(y1);
+    *reinterpret_cast<bf16x8*>(dst + i0) = pack8(y0);
+    *reinterpret_cast<bf16x8*>(dst + 64 + i0) = pack8(y1);
   }
   // v: straight copy, 8 elements per item
   const int n_v = a.hkv * kHeadDim / 8;
