@@ -188,6 +188,10 @@ def main() -> None:
                     help="tensor-parallel size of each engine replica (config 5: 2); "
                          "replicas are rank pairs (2i, 2i+1), placement applies to replicas")
     args = ap.parse_args()
+    if os.environ.get("CORTEX_DUMP_AFTER"):  # debugging stuck runs: periodic stack dumps
+        import faulthandler
+
+        faulthandler.dump_traceback_later(float(os.environ["CORTEX_DUMP_AFTER"]), repeat=True)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -220,6 +224,10 @@ def main() -> None:
     backend = os.environ.get("CORTEX_DIST_BACKEND", "nccl")
     if backend != "nccl":
         local %= torch.cuda.device_count()
+        # ranks time-sliced on a shared GPU: programmatic dependent launch off (with it,
+        # 2 of 6 disjoint N = 2 runs on one GPU hung; without it 6 of 6 completed,
+        # DESIGN.md §6.1); one process per GPU keeps it on
+        os.environ.setdefault("CORTEX_PDL", "0")
     comm_dev = torch.device("cuda", local) if backend == "nccl" else torch.device("cpu")
     if world > 1:
         import torch.distributed as dist

@@ -226,6 +226,7 @@ class GpuWorker:
         self.launches = 0  # kernels of this library launched since construction
         self.steps = 0
         self.on_forward = None  # optional hook(plan, n_out) for parity checking
+        self.check_finite = os.environ.get("CORTEX_CHECK_FINITE") == "1"  # debug only
         # TP: optional host hook at every exchange point (device sync + a host barrier) so
         # that two ranks sharing one GPU never have a kernel waiting on the other rank
         self.tp_sync = None
@@ -335,7 +336,29 @@ class GpuWorker:
         for _ in self.forward_steps(plan):
             if self.tp_sync is not None:  # functional TP runs with both ranks on one GPU
                 self.tp_sync()
+        if self.check_finite:
+            self._check_finite(plan)
         return self.n_out
+
+    def _check_finite(self, plan: StepPlan) -> None:
+        """Debug mode (CORTEX_CHECK_FINITE=1): synchronise after every step and fail with
+        the step's plan when an output row's logits are not all finite."""
+        bad = (~torch.isfinite(self.logits[: self.n_out])).any(dim=1).nonzero().flatten()
+        if bad.numel() == 0:
+            return
+        rows = bad.tolist()[:8]
+        lines = [f"non-finite logits in {bad.numel()} of {self.n_out} output rows {rows}"]
+        for r in rows:
+            if r < len(plan.decode):
+                d = plan.decode[r]
+                lines.append(f"  decode row {r}: table row {d.row} prefix {d.prefix_len} "
+                             f"kv_len {d.kv_len} hist_pos {d.hist_pos} prefix_key "
+                             f"{d.prefix_key}")
+            else:
+                lines.append(f"  prefill output row {r}")
+        lines.append(f"  decode {len(plan.decode)}, prefill "
+                     f"{[(s.row, s.prefix_len, s.kv_len, len(s.tokens)) for s in plan.prefill]}")
+        raise FloatingPointError("\n".join(lines))
 
     @torch.no_grad()
     def forward_steps(self, plan: StepPlan):
