@@ -109,7 +109,9 @@ def _free_port() -> int:
 def _ipc_rank(rank: int, port: int, out_dir: str) -> None:
     import torch.distributed as dist
 
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    # both ranks are time-sliced on one GPU: programmatic dependent launch off there
+    # ("Several runtimes time-sliced on ONE GPU"); results do not depend on it
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), CORTEX_PDL="0")
     dist.init_process_group("gloo", rank=rank, world_size=2)
     dev = torch.device("cuda:0")
     torch.cuda.set_device(dev)
