@@ -511,6 +511,16 @@ void cortex_gemm2_plan(int M, int N, int K, int n_sms, int* tn_out, int* sk_out)
     g_sk_force = e ? atoi(e) : -1;
   }
   const int force = g_sk_force == 1 ? 1 : 0;
+  static int tn_force = -2;  // tuning hook: CORTEX_GEMM_TN pins the token tile width
+  if (tn_force == -2) {
+    const char* e = getenv("CORTEX_GEMM_TN");
+    tn_force = e ? atoi(e) : -1;
+  }
+  if (tn_force > 0) {
+    *tn_out = tn_force;
+    *sk_out = force;
+    return;
+  }
   const int n_tiles = N / kPairN;
   const int pairs = n_sms / 2;
   double best = -1.0;
