@@ -219,7 +219,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
-  pdl_wait();  // the activations (and residual) come from the previous kernel
+  // The weights are immutable: their producer (warp 0) fills the pipeline while the
+  // previous kernel of the stream is still running; everyone else waits for it first
+  // (the activations and residual come from it, and the outputs may alias its inputs).
+  if (warp != 0) pdl_wait();
   pdl_trigger();
 
   if (warp == 0) {
@@ -246,6 +249,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         }
       }
     }
+    pdl_wait();  // nothing below touches memory, but keep every thread ordered
   } else if (warp == 6) {
     if (elect_one()) {
       // ---- second TMA issuer: the token rows. A TMA-issuing thread's copies complete

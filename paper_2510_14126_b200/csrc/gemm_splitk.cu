@@ -199,8 +199,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   SK_TRACE(1);
-  pdl_wait();  // the activations (and residual) come from the previous kernel
-  pdl_trigger();
   const uint16_t pair_mask = static_cast<uint16_t>(3u << lead);
 
   // ---- TMA issuers. The copies one thread issues complete one after another, so the
@@ -213,6 +211,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int w_idx = warp == 0 ? 0 : (warp == 3 && n_w == 2 ? 1 : -1);
   const int x_idx = args.n_issue == 1 ? (warp == 0 ? 0 : -1)
                                       : (warp == 2 ? 0 : (warp == 4 && n_w == 2 ? 1 : -1));
+  // The weights are immutable: a weights-only issuer fills the pipeline while the
+  // previous kernel of the stream is still running, and waits for it afterwards (its
+  // warp may drain partials into the workspace the previous kernel reads). Everyone
+  // else waits first: the activations (and residual) come from that kernel.
+  const bool w_only = w_idx >= 0 && x_idx < 0;
+  if (!w_only) pdl_wait();
+  pdl_trigger();
   if ((w_idx >= 0 || x_idx >= 0) && elect_one()) {
     const int n0 = n_tile * kPairN * NW + static_cast<int>(rank) * 128;
     const int x0 = m_tile * TN + static_cast<int>(rank) * (TN / 2);
@@ -274,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
+  if (w_only) pdl_wait();
   __syncwarp();  // reconverge the issuing lanes before the warp-collective TMEM loads
   const int m0 = m_tile * TN;
   const int rows = min(TN, args.M - m0);
