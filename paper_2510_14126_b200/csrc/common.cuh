@@ -43,6 +43,18 @@ extern int g_cortex_pdl;
 CORTEX_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 CORTEX_DEVICE void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" :::); }
 
+// L2 prefetch of one 2-D tensor-map box (no shared memory, no barrier).
+CORTEX_DEVICE void tma_prefetch_l2_2d(const void* desc, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(desc)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+
+// K blocks of weights a GEMM's weights-only issuer prefetches into L2, beyond its
+// pipeline stages, before the PDL wait (CORTEX_GEMM_L2PF tuning hook; default 0 = off).
+int cortex_gemm_l2pf();
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                               cudaStream_t stream, int cluster_x, Args&&... args) {

@@ -50,6 +50,7 @@ struct Gemm2Args {
   int total_units;   // num_tiles * K blocks
   float* workspace;  // stream-K: [npairs * 2][TN][128] fp32 partials
   int* flags;        // stream-K: [npairs * 2] partial-ready flags, left zeroed
+  int l2pf;          // weight K blocks prefetched into L2 beyond the stages (first segment)
 };
 
 struct Seg {
@@ -231,11 +232,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       uint32_t it = 0;
       int pos = seg_start(args, pair);
       Seg g;
+      bool first = true;
       while (seg_next(args, pair, pos, g)) {
         const int n_tile = g.t / args.m_tiles;
         const int m_tile = g.t % args.m_tiles;
         (void)m_tile;
         const int n0 = n_tile * kPairN + rank * 128;
+        if (first) {  // the K blocks after the first STAGES: into L2 before the wait
+          const int pf1 = min(g.kb1, g.kb0 + STAGES + args.l2pf);
+          for (int kb = g.kb0 + STAGES; kb < pf1; ++kb) tma_prefetch_l2_2d(&tmap_w, kb * kBK, n0);
+          first = false;
+        }
         for (int kb = g.kb0; kb < g.kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
@@ -592,6 +599,7 @@ int32_t cortex_gemm_2sm_launch(const void* tmap_w, const void* tmap_x, int32_t M
   a.total_units = num_tiles * (K / kBK);
   a.workspace = workspace;
   a.flags = counters;
+  a.l2pf = cortex_gemm_l2pf();
   const auto* tw = reinterpret_cast<const CUtensorMap*>(tmap_w);
   const auto* tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
   switch (tn) {

@@ -43,6 +43,7 @@ struct SkArgs {
   int m_tiles;
   float* ws;    // [tiles][ks][2][TN][128] fp32 partials
   int n_issue;  // TMA issuing threads: 1, 2 (weights | tokens) or 4 (two of each)
+  int l2pf;     // weight K blocks prefetched into L2 beyond the stages, before the PDL wait
 };
 
 // NW weight sub-tiles of 256 rows per pair (one MMA each, sharing the staged token rows):
@@ -220,6 +221,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_trigger();
   if ((w_idx >= 0 || x_idx >= 0) && elect_one()) {
     const int n0 = n_tile * kPairN * NW + static_cast<int>(rank) * 128;
+    if (w_idx == 0 && w_only) {
+      // the K blocks after the first STAGES: into L2 while the predecessor runs
+      const int pf1 = min(kb1, kb0 + STAGES + args.l2pf);
+      for (int kb = kb0 + STAGES; kb < pf1; ++kb)
+#pragma unroll
+        for (int w = 0; w < NW; ++w) tma_prefetch_l2_2d(&tmap_w, kb * kBK, n0 + w * kPairN);
+    }
     const int x0 = m_tile * TN + static_cast<int>(rank) * (TN / 2);
     const uint64_t pol_w = policy_evict_first();  // weights: streamed once per step
     for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
@@ -373,6 +381,16 @@ int g_sk_issue = -2;
 
 }  // namespace
 
+int cortex_gemm_l2pf() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CORTEX_GEMM_L2PF");
+    v = e ? atoi(e) : 0;  // measured: 0 best (profiles/r1e_gemm_l2pf_sweep.jsonl)
+    if (v < 0) v = 0;
+  }
+  return v;
+}
+
 extern "C" {
 
 // Plan of the split-K kernel for (M, N, K): returns ks (>= 2) and writes the token tile
@@ -478,6 +496,7 @@ int32_t cortex_gemm_splitk_launch(const void* tmap_w, const void* tmap_x, int32_
     if (g_sk_issue != 1 && g_sk_issue != 4) g_sk_issue = 2;
   }
   a.n_issue = g_sk_issue;
+  a.l2pf = cortex_gemm_l2pf();
   const auto* tw = reinterpret_cast<const CUtensorMap*>(tmap_w);
   const auto* tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
   if (nw == 2) {
