@@ -460,8 +460,11 @@ CORTEX_DEVICE int tile_nvalid(int prefix, int kvlen, int j) {
 
 __global__ void __launch_bounds__(kWarps * 32)
     paged_decode_kernel(const __grid_constant__ CUtensorMap tmap_kv, const DecodeArgs a) {
-  pdl_wait();
-  pdl_trigger();
+  // Before the PDL wait this kernel reads only what earlier steps or earlier kernels of
+  // this step wrote (call metadata, block table, the KV of past tokens): every kernel of
+  // the stream waits for its own predecessor before it triggers, so only the immediate
+  // predecessor (RoPE / KV append: q and the new token's K/V in the call's last tile)
+  // can still be running. The last tile's load and q wait for it.
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -474,7 +477,11 @@ __global__ void __launch_bounds__(kWarps * 32)
   const int ntiles = num_tiles(prefix, kvlen);
   const int first_tile = a.cascade ? (prefix + kTile - 1) / kTile : 0;
   const int t_begin = first_tile + split * kTilesPerSplit;
-  if (t_begin >= ntiles) return;
+  if (t_begin >= ntiles) {
+    pdl_wait();
+    pdl_trigger();
+    return;
+  }
   const int t_end = min(ntiles, t_begin + kTilesPerSplit);
   const int warp = warp_id();
   const int lane = lane_id();
@@ -493,13 +500,22 @@ __global__ void __launch_bounds__(kWarps * 32)
   static_assert(kTilesPerSplit / kWarps <= 32, "block ids are held one per lane");
   const int my_blk = lane < n_mine ? __ldg(&table_row[t_begin + warp + kWarps * lane]) : 0;
   __syncwarp();
+  int deferred = -1;  // stage of the last tile (the new token's K/V), loaded after the wait
 #pragma unroll
   for (int i = 0; i < kDecodeStages; ++i) {
     const int blk = __shfl_sync(0xffffffffu, my_blk, i);
-    if (lane == 0 && i < n_mine)
+    if (i < n_mine && t_begin + warp + kWarps * i == ntiles - 1)
+      deferred = i;
+    else if (lane == 0 && i < n_mine)
       load_tile(my_stages + i * kStageBytes, &tmap_kv, &bars[i], a.k_row0, a.v_row0, blk, kvh,
                 a.n_kv_heads);
   }
+  pdl_wait();
+  pdl_trigger();
+  const int dblk = __shfl_sync(0xffffffffu, my_blk, deferred >= 0 ? deferred : 0);
+  if (deferred >= 0 && lane == 0)
+    load_tile(my_stages + deferred * kStageBytes, &tmap_kv, &bars[deferred], a.k_row0, a.v_row0,
+              dblk, kvh, a.n_kv_heads);
 
   uint32_t qb[8][2];
   load_q_cols(qb, a.q, (static_cast<int64_t>(b) * hq + kvh * a.group) * kHeadDim, a.group);
