@@ -382,6 +382,8 @@ class TpFollower:
             elif name in ("copy_prefix_row", "copy_first_token"):
                 getattr(w, name)(*op[1:])
             elif name == "collective":
+                if op[1] == "arm":  # a new topology arm: fresh engine slices (bitmaps all free)
+                    self.pools.clear()
                 if self.on_collective is None:
                     raise RuntimeError("leader issued a collective the follower cannot join")
                 self.on_collective(op[1], op[2])

@@ -142,15 +142,6 @@ class Workflow:
         o = self.spec.output_tokens.sample_int(self._draw("output", self.stage))
         return p, o
 
-    def replay_to(self, stage: str) -> None:
-        """Re-derive the state at the first entry of `stage` from the rid alone (every
-        draw is a counter stream keyed by (rid, stage, visit)); used by the rank a
-        workflow is handed to under disjoint placement (placement.py)."""
-        while self.stage != stage:
-            self.enter()
-            if self.finish() is None:
-                raise ValueError(f"request {self.rid} ends before reaching {stage}")
-
     def finish(self) -> str | None:
         """Apply the current stage's outcome; returns the next stage or None when done."""
         outs = self.spec.outcomes(self.stage)

@@ -26,6 +26,10 @@ Fixtures
       engines, Poisson rate 2.0, 96 workflows (ELASTIC below). The call stream
       adds "create" (autoscale scale-out / start-up) and "retire" (scale-in)
       records; audit.json holds the reference's borrow / return / scale events.
+  evict/{dispatch,requests,kv_usage}.csv + summary.json + engine_calls.jsonl
+      AC-2's tight shared topology (EVICT below): two shared engines of 3200
+      tokens each, so routing evicts idle stage prefixes (route_call_with_eviction,
+      scheduling.py:143-165 -> evict_idle_prefix, engines.py:219-226).
   trace_seed0_{n}_pf{p}.json
       per-workflow stage/retry outcomes (prompt/output tokens per LLM visit,
       terminal, retries) for n workflows, computed by the reference Simulator.
@@ -228,6 +232,39 @@ def gen_elastic() -> None:
           "borrows:", len(a.borrows), "scale events:", len(a.scale_events))
 
 
+EVICT = {"engines": (1, 1), "rate": 2.1, "cap": 96, "seed": 2,
+         "params": (3200, 2000.0, 0.02, 0.1, 12)}
+
+
+def evict_config():
+    """AC-2's tight shared topology (pkg/tests/test_acceptance.py:79-99: capacity 3200 =
+    2P + room for ~4 calls, max_batch 12, prefill 2000 tok/s, rate 2.1) over 2 shared
+    engines: an engine holding the other stage's idle prefix must evict it
+    (scheduling.py:143-165 -> engines.py:219-226) before it can admit."""
+    import dataclasses
+
+    cfg = config1(seed=EVICT["seed"], engines=EVICT["engines"], mode="shared",
+                  params=EngineParams(*EVICT["params"]))
+    return dataclasses.replace(cfg, arrival_rate=EVICT["rate"])
+
+
+def gen_evict() -> None:
+    out = HERE / "evict"
+    if out.exists():
+        shutil.rmtree(out)
+    RecordingEngine.log = []
+    cls = type("Rec", (CappedSimulator,), {"engine_cls": RecordingEngine, "cap": EVICT["cap"]})
+    sim = cls(evict_config())
+    result = sim.run()
+    write_run_outputs(result, out)
+    with (out / "engine_calls.jsonl").open("w") as f:
+        for rec in RecordingEngine.log:
+            f.write(json.dumps(rec, sort_keys=True) + "\n")
+    n_ev = sum(1 for r in RecordingEngine.log if r["op"] == "evict_idle_prefix")
+    print("evict:", result.report.summary_line(), "calls:", len(RecordingEngine.log),
+          "evictions:", n_ev)
+
+
 def gen_traces() -> None:
     for n, pf in ((64, 0.5), (1024, 0.5), (1024, 0.6)):
         cls = type("Cap", (CappedSimulator,), {"cap": n})
@@ -377,4 +414,5 @@ if __name__ == "__main__":
     gen_engine_scenarios()
     gen_config1()
     gen_elastic()
+    gen_evict()
     gen_traces()

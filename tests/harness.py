@@ -27,6 +27,9 @@ from paper_2510_14126_b200.engine import (
 GOLDEN = Path(__file__).resolve().parent / "golden"
 CONFIG1_PARAMS = EngineParams(16384, 5000.0, 0.02, 0.1, 8)
 CONFIG1_POOLS = {0: "pool:sql_generator", 1: "pool:sql_fixer"}
+# tests/golden/evict: AC-2's tight shared topology (make_golden.EVICT)
+EVICT_PARAMS = EngineParams(3200, 2000.0, 0.02, 0.1, 12)
+EVICT_POOLS = {0: "pool:llm", 1: "pool:llm"}
 
 
 def engine_state(e) -> dict:
@@ -173,10 +176,15 @@ class HostWorker(FakeWorker):
         return len(plan.decode) + sum(len(s.tokens) for s in plan.prefill)
 
 
-def config1_engines(worker, observer=None, seed: int = 0, vocab: int = 1024):
-    params = CONFIG1_PARAMS
+def golden_engines(worker, params, pools: dict, observer=None, seed: int = 0,
+                   vocab: int = 1024):
+    """Engines 0..n-1 on consecutive slices of `worker` (block ids [e*bpe, (e+1)*bpe))."""
     bpe = blocks_for(params)
     tokens = TokenSource(seed, vocab)
-    slices = make_slices(worker, 2, bpe, params.max_batch, tokens)
-    engines = {i: GpuEngineState(i, params, CONFIG1_POOLS[i], slices[i], observer) for i in range(2)}
+    slices = make_slices(worker, len(pools), bpe, params.max_batch, tokens)
+    engines = {i: GpuEngineState(i, params, pools[i], slices[i], observer) for i in pools}
     return engines, bpe
+
+
+def config1_engines(worker, observer=None, seed: int = 0, vocab: int = 1024):
+    return golden_engines(worker, CONFIG1_PARAMS, CONFIG1_POOLS, observer, seed, vocab)

@@ -30,11 +30,11 @@ ELASTIC = GOLDEN / "elastic"
 class FakeArena(FakeWorker):
     """FakeWorker with the arena shape gpu_engine_factory carves."""
 
-    def __init__(self, n_engines: int) -> None:
+    def __init__(self, n_engines: int, params=CONFIG1_PARAMS) -> None:
         import types
 
-        bpe = blocks_for(CONFIG1_PARAMS)
-        super().__init__(n_engines * bpe, n_engines * (CONFIG1_PARAMS.max_batch + 4))
+        bpe = blocks_for(params)
+        super().__init__(n_engines * bpe, n_engines * (params.max_batch + 4))
         self.table = np.zeros((self.table.shape[0], bpe), np.int32)
         self.cfg = types.SimpleNamespace(vocab=1024)
 
@@ -124,3 +124,27 @@ def test_reference_simulator_elastic_host(tmp_path):
         kv_used = float(q.split(",")[3])
         # the blocks cover the materialised tokens (floor of each call's emitted count)
         assert int(nb) * 16 >= kv_used - CONFIG1_PARAMS.max_batch
+
+
+def test_reference_simulator_evict_host(tmp_path):
+    """AC-2's tight shared topology (tests/golden/evict): the reference Simulator's own
+    routing evicts idle prefixes on GpuEngineState engines (device half recorded); its
+    outputs equal the golden byte for byte and every eviction frees the prefix blocks."""
+    if not _stagesim():
+        pytest.skip("reference package not importable")
+    sys.path.insert(0, str(GOLDEN))
+    from make_golden import EVICT, CappedSimulator, evict_config
+    from stagesim.reporting import write_run_outputs
+
+    from harness import EVICT_PARAMS
+
+    worker = FakeArena(2, EVICT_PARAMS)
+    factory = gpu_engine_factory(worker, EVICT_PARAMS, seed=0)
+    sim = gpu_simulator(type("Cap", (CappedSimulator,), {"cap": EVICT["cap"]}), factory)(
+        evict_config())
+    result = sim.run()
+    write_run_outputs(result, tmp_path)
+    for name in ("dispatch.csv", "requests.csv", "kv_usage.csv", "summary.json"):
+        assert filecmp.cmp(tmp_path / name, GOLDEN / "evict" / name, shallow=False), name
+    prefix_frees = [e for e in worker.log if e[0] == "free" and e[2][0][1] == 0]
+    assert len(prefix_frees) == 12

@@ -16,12 +16,15 @@ import pytest
 
 from harness import (
     CONFIG1_PARAMS,
+    EVICT_PARAMS,
+    EVICT_POOLS,
     GOLDEN,
     FakeWorker,
     RecordingObserver,
     config1_engines,
     engine_state,
     find_call,
+    golden_engines,
     load_jsonl,
     replay_calls,
 )
@@ -119,6 +122,28 @@ def test_config1_call_stream_matches_reference():
     for eid in (0, 1):
         for c in obs.completed[eid]:
             assert c["have"] == max(1, c["o"])
+
+
+def test_evict_call_stream_matches_reference():
+    """AC-2's tight shared topology (tests/golden/evict): the reference routes with
+    eviction (scheduling.py:143-165), so its stream holds evict_idle_prefix calls
+    (engines.py:219-226); replayed bit for bit, the prefix frees follow the contract."""
+    records = load_jsonl(GOLDEN / "evict" / "engine_calls.jsonl")
+    n_ev = sum(1 for r in records if r["op"] == "evict_idle_prefix")
+    assert n_ev >= 10
+    worker = FakeWorker(4 * blocks_for(EVICT_PARAMS), 64)
+    obs = RecordingObserver(read_device=False)
+    engines, bpe = golden_engines(worker, EVICT_PARAMS, EVICT_POOLS, obs)
+    checks = replay_calls(records, engines)
+    assert checks > 2000
+    ref = replay_blocks(records, {0: (bpe, 0), 1: (bpe, bpe)})
+    for eid in (0, 1):
+        assert obs.allocs[eid] == ref[eid].alloc_log, eid
+        assert [c["rid"] for c in obs.completed[eid]] == [c["rid"] for c in ref[eid].completed]
+    # every eviction freed exactly the evicted stage's prefix blocks (row, col 0, ceil(P/16))
+    prefix_frees = [e for e in worker.log if e[0] == "free" and e[2][0][1] == 0]
+    assert len(prefix_frees) == n_ev
+    assert all(e[2][0][2] == 63 for e in prefix_frees)  # P = 1000 -> 63 blocks
 
 
 def test_no_cpu_fallback():

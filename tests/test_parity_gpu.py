@@ -29,9 +29,12 @@ import torch
 
 from harness import (
     CONFIG1_PARAMS,
+    EVICT_PARAMS,
+    EVICT_POOLS,
     GOLDEN,
     RecordingObserver,
     config1_engines,
+    golden_engines,
     load_jsonl,
     replay_calls,
 )
@@ -48,10 +51,11 @@ LOGIT_TOL = 2e-3
 TIE_TOL = 2e-2  # absolute logit units; logits here have |max| ~ 1
 
 
-def _worker(cuda, n_engines=2):
-    bpe = blocks_for(CONFIG1_PARAMS)
-    return GpuWorker(TINY, cuda, n_blocks=n_engines * bpe, n_rows=n_engines * 12, row_cols=bpe,
-                     max_tokens=2048, max_out=64, hist_cols=512, max_seq_tokens=16384 + 64)
+def _worker(cuda, n_engines=2, params=CONFIG1_PARAMS):
+    bpe = blocks_for(params)
+    return GpuWorker(TINY, cuda, n_blocks=n_engines * bpe,
+                     n_rows=n_engines * (params.max_batch + 4), row_cols=bpe, max_tokens=2048,
+                     max_out=64, hist_cols=512, max_seq_tokens=16384 + 64)
 
 
 class LogitCapture:
@@ -154,22 +158,28 @@ def test_config1_engine_parity(cuda):
 
 
 def _stagesim():
+    """Make the installed reference package importable; fail (not skip) without it.
+
+    The reference is installed by `__graft_entry__.build()` into baseline/_ref (git-
+    ignored, travels to the GPU box with the snapshot); any directory under it holding
+    a `stagesim` package is accepted, then site-packages."""
     root = Path(__file__).resolve().parents[1]
-    for cand in (root / "baseline" / "_ref", Path("/root/reference/pkg/src")):
-        if (cand / "stagesim").exists() and str(cand) not in sys.path:
+    base = root / "baseline" / "_ref"
+    cands = [p.parent for p in sorted(base.rglob("stagesim/__init__.py"))] if base.exists() else []
+    for cand in cands:
+        if str(cand) not in sys.path:
             sys.path.insert(0, str(cand))
+        break
     try:
         import stagesim  # noqa: F401
-
-        return True
     except ImportError:
-        return False
+        pytest.fail("reference package stagesim not importable: run __graft_entry__.build() "
+                    "(installs it into baseline/_ref) before the GPU tests")
 
 
 def test_reference_simulator_drives_gpu_engines(cuda, tmp_path):
     """Drop-in: the reference Simulator itself, engines swapped at its factory seam."""
-    if not _stagesim():
-        pytest.skip("reference package not importable on this box")
+    _stagesim()
     sys.path.insert(0, str(GOLDEN))
     from make_golden import CappedSimulator, config1  # the fixture generator's own harness
     from stagesim.reporting import write_run_outputs
@@ -204,8 +214,7 @@ def test_elastic_reference_simulator_gpu(cuda, tmp_path):
     scale-out and closed on scale-in; outputs byte-identical, block tables equal the
     oracle's, retired slices return every block, borrowed calls' tokens match the
     decoder oracle (the generator prefix re-materialised on a lent fixer engine)."""
-    if not _stagesim():
-        pytest.skip("reference package not importable on this box")
+    _stagesim()
     sys.path.insert(0, str(GOLDEN))
     import json
 
@@ -267,3 +276,80 @@ def test_elastic_reference_simulator_gpu(cuda, tmp_path):
                 logits = seq.extend([c["tokens"][k - 1]])
             if greedy(logits) != t:
                 assert top2_margin(logits) < TIE_TOL, (c["rid"], k)
+
+
+def test_evict_engine_parity_gpu(cuda):
+    """Prefix eviction on GPU engines (tests/golden/evict: AC-2's tight shared topology,
+    12 evict_idle_prefix calls of the reference's own stream, engines.py:219-226 reached
+    via route_call_with_eviction, scheduling.py:143-165): engine state bit-exact after
+    every call, every completed call's block row equals the oracle's (re-planted prefixes
+    land on the blocks the eviction freed), device free counts equal the oracle's, and
+    the greedy tokens of the calls admitted cold right after an eviction match the CPU
+    decoder oracle."""
+    records = load_jsonl(GOLDEN / "evict" / "engine_calls.jsonl")
+    worker = _worker(cuda, params=EVICT_PARAMS)
+    obs = RecordingObserver(read_device=True)
+    engines, bpe = golden_engines(worker, EVICT_PARAMS, EVICT_POOLS, obs, vocab=TINY.vocab)
+    replay_calls(records, engines)
+    torch.cuda.synchronize()
+    assert int(worker.status[0]) == 0
+    ref = replay_blocks(records, {0: (bpe, 0), 1: (bpe, bpe)})
+    from paper_2510_14126_b200 import ops
+
+    n_calls = 0
+    for eid in (0, 1):
+        got, exp = obs.completed[eid], ref[eid].completed
+        assert [g["rid"] for g in got] == [e["rid"] for e in exp]
+        for g, e in zip(got, exp):
+            assert g["row"] == e["row"], (eid, g["rid"])
+            n_calls += 1
+        n_free = torch.zeros(1, dtype=torch.int32, device=cuda)
+        ops.kv_count_free(engines[eid].gpu.bitmap, bpe, n_free)
+        assert int(n_free[0]) == ref[eid].pool.n_free()
+    assert n_calls == sum(1 for r in records if r["op"] == "complete_call")
+    # calls admitted cold right after an eviction on the same engine
+    after = []
+    pending = set()
+    for r in records:
+        if r["op"] == "evict_idle_prefix":
+            pending.add(r["eng"])
+        elif r["op"] == "admit" and r["eng"] in pending:
+            pending.discard(r["eng"])
+            after.append((r["eng"], r["args"][0]["request_id"], r["args"][0]["stage_id"]))
+    assert len(after) >= 10
+    dec = RefDecoder(TINY.to_ref(), worker.oracle_weights(), max_pos=4096)
+    checked = 0
+    for eid, rid, sid in after[:4]:
+        c = next(x for x in obs.completed[eid] if x["rid"] == rid and x["sid"] == sid)
+        seq = dec.new_seq()
+        seq.extend(prefix_tokens(0, sid, c["P"], TINY.vocab), "none")
+        logits = seq.extend(prompt_tokens(0, rid, sid, c["visit"], c["p"], TINY.vocab))
+        for k, t in enumerate(c["tokens"]):
+            if k:
+                logits = seq.extend([c["tokens"][k - 1]])
+            if greedy(logits) != t:
+                assert top2_margin(logits) < TIE_TOL, (rid, k)
+            checked += 1
+    assert checked > 100
+
+
+def test_evict_reference_simulator_gpu(cuda, tmp_path):
+    """The reference Simulator (shared topology, tight capacity) driving GPU engines:
+    its routing evicts idle prefixes on the GPU engines; outputs byte-identical."""
+    _stagesim()
+    sys.path.insert(0, str(GOLDEN))
+    from make_golden import CappedSimulator, EVICT, evict_config
+    from stagesim.reporting import write_run_outputs
+
+    from paper_2510_14126_b200.integration import gpu_engine_factory, gpu_simulator
+
+    worker = _worker(cuda, params=EVICT_PARAMS)
+    factory = gpu_engine_factory(worker, EVICT_PARAMS, seed=0)
+    sim = gpu_simulator(type("Cap", (CappedSimulator,), {"cap": EVICT["cap"]}), factory)(
+        evict_config())
+    result = sim.run()
+    write_run_outputs(result, tmp_path)
+    torch.cuda.synchronize()
+    assert int(worker.status[0]) == 0
+    for name in ("dispatch.csv", "requests.csv", "kv_usage.csv", "summary.json"):
+        assert filecmp.cmp(tmp_path / name, GOLDEN / "evict" / name, shallow=False), name

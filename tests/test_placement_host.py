@@ -1,7 +1,13 @@
-"""Disjoint generator/fixer placement (placement.py) on CPU: world_size 2 over gloo,
-host-only workers. Checks that handing workflows across ranks reproduces the
-single-rank outcomes exactly (the same terminal states and stage histories) and
-that the closed loop keeps its concurrency bound."""
+"""Stage pools across replicas (cluster.py + runtime.py) on CPU: gloo process groups,
+host-only workers.
+
+Checked: the placement of engines into pools (isolated with any generator:fixer split,
+shared), the shared-memory link rings, and that serving the seeded NL2SQL trace with
+the pools' engines spread over 2, 3 and 4 processes (routing over every engine of a
+pool from the scheduler on replica 0) reproduces the single-process outcomes exactly
+(terminal states and stage histories are a pure function of the request id,
+stagesim/rng.py:17-20), keeps the closed loop's concurrency bound and uses every engine.
+"""
 
 from __future__ import annotations
 
@@ -12,37 +18,41 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2510_14126_b200.engine import EngineParams, blocks_for
-from paper_2510_14126_b200.placement import (
-    ROLE_BOTH,
-    ROLE_FIXER,
-    ROLE_GENERATOR,
-    PairChannel,
-    open_pair_channel,
-    role_of,
-)
-from paper_2510_14126_b200.runtime import PoolRuntime
-from paper_2510_14126_b200.workflow import FIXER, Nl2Sql
-
 from harness import HostWorker
+from paper_2510_14126_b200.cluster import (
+    CMD_ADMIT,
+    POOL_FIXER,
+    POOL_GENERATOR,
+    POOL_SHARED,
+    EngineSpec,
+    ReplicaLink,
+    open_links,
+    parse_split,
+    plan_engines,
+)
+from paper_2510_14126_b200.engine import EngineParams, blocks_for
+from paper_2510_14126_b200.runtime import PoolRuntime, ReplicaExecutor, ReplicaServer
+from paper_2510_14126_b200.workflow import FIXER, Constant, Nl2Sql
 
 N_WF = 48
 CONC = 8
 
 
-def _runtime(role, channel, n_eng):
-    params = EngineParams(1000 + CONC * 450, 5000.0, 0.02, 0.1, CONC)
-    bpe = blocks_for(params)
-    w = HostWorker(n_eng * bpe, n_eng * (CONC + 4))
-    spec = Nl2Sql(retry_budget=5, executor_service_time=_fast_exec())
-    return PoolRuntime(w, spec, params, concurrency=CONC, n_workflows=N_WF, seed=0,
-                       prefill_budget=2048, role=role, channel=channel)
+def _params(max_batch=CONC):
+    return EngineParams(2 * 1000 + max_batch * 450, 5000.0, 0.02, 0.1, max_batch)
 
 
-def _fast_exec():
-    from paper_2510_14126_b200.workflow import Constant
+def _spec():
+    return Nl2Sql(retry_budget=5, executor_service_time=Constant(0.0))
 
-    return Constant(0.0)
+
+MB = 3  # multi-replica runs: engine batches below the concurrency, so a pool spills
+        # onto its next engine (warm-first routing would otherwise keep one engine busy)
+
+
+def _host_worker(n_eng, max_batch=CONC):
+    p = _params(max_batch)
+    return HostWorker(max(n_eng, 1) * blocks_for(p), max(n_eng, 1) * (CONC + 4))
 
 
 def _summary(rt):
@@ -57,81 +67,115 @@ def _free_port() -> int:
     return port
 
 
-def _worker(rank, world, port, q):
+def test_plan_engines():
+    assert plan_engines("isolated", 1) == [EngineSpec(0, POOL_GENERATOR, 0),
+                                           EngineSpec(1, POOL_FIXER, 0)]
+    assert plan_engines("shared", 1) == [EngineSpec(0, POOL_SHARED, 0),
+                                         EngineSpec(1, POOL_SHARED, 0)]
+    eight = plan_engines("isolated", 8)  # configs 3 / 4: generator 4 GPUs, fixer 4 GPUs
+    assert [e.pool for e in eight] == [POOL_GENERATOR] * 4 + [POOL_FIXER] * 4
+    assert [e.replica for e in eight] == list(range(8))
+    c5 = plan_engines("isolated", 8, parse_split("2:6", 8))  # config 5's widest fixer pool
+    assert [e.pool for e in c5] == [POOL_GENERATOR] * 2 + [POOL_FIXER] * 6
+    c5tp = plan_engines("isolated", 4, parse_split("1:3", 4))  # TP = 2: 4 replicas on 8 GPUs
+    assert [e.pool for e in c5tp] == [POOL_GENERATOR] + [POOL_FIXER] * 3
+    assert [e.pool for e in plan_engines("shared", 8)] == [POOL_SHARED] * 8
+    with pytest.raises(ValueError):
+        parse_split("0:8", 8)
+    with pytest.raises(ValueError):
+        parse_split("3:4", 8)
+
+
+def test_link_rings():
+    link = ReplicaLink(f"cortex_test_{os.getpid()}", create=True, cap=4, n_engines=2)
+    try:
+        for i in range(3):
+            link.cmd.push(CMD_ADMIT, 1, i, 0, 0, 100, 50, 1000)
+        got = link.cmd.pop_all()
+        assert [r[2] for r in got] == [0, 1, 2] and got[0][:8] == (CMD_ADMIT, 1, 0, 0, 0, 100,
+                                                                   50, 1000)
+        assert link.cmd.pop_all() == []
+        for i in range(4):  # wraps
+            link.evt.push(1, 0, 10 + i, 1)
+        with pytest.raises(RuntimeError):
+            link.evt.push(1, 0, 99, 1)
+        assert [r[2] for r in link.evt.pop_all()] == [10, 11, 12, 13]
+        link.stat_f[1, 0] = 12.5
+        link.stat[1, 1] = 7
+        assert float(link.stat_f[1, 0]) == 12.5 and int(link.stat[1, 1]) == 7
+        link.phase = 3
+        assert link.phase == 3
+    finally:
+        link.close()
+
+
+def _single(mode):
+    rt = PoolRuntime(_host_worker(2), _spec(), _params(), mode=mode, concurrency=CONC,
+                     n_workflows=N_WF, seed=0, prefill_budget=2048)
+    rt.fill()
+    rt.run_until(N_WF, max_seconds=120)
+    return _summary(rt)
+
+
+def _replica_proc(rank, world, port, mode, split, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    role, _, _ = role_of(rank, world)
-    ch = open_pair_channel(dist, rank, world, cap=4 * CONC)
-    rt = _runtime(role, ch, 1)
-    rt.fill()
-    if role == ROLE_GENERATOR:
+    specs = plan_engines(mode, world, split)
+    mine = [s for s in specs if s.replica == rank]
+    links = open_links(dist, rank, world, specs, cap=4 * CONC + 64)
+    if rank == 0:
+        rt = PoolRuntime(_host_worker(len(mine), MB), _spec(), _params(MB), mode=mode,
+                         concurrency=CONC, n_workflows=N_WF, seed=0, prefill_budget=2048,
+                         engines=specs, links=links)
+        rt.fill()
         max_inflight = 0
-        while rt._next_rid_i < N_WF or rt.workflows or rt.remote:
-            rt.step()
-            max_inflight = max(max_inflight, len(rt.workflows) + rt.remote)
-        ch.phase = 1
-    else:
-        max_inflight = 0
-        while ch.phase == 0:
+        while rt.workflows:
             rt.step()
             max_inflight = max(max_inflight, len(rt.workflows))
-        rt.step()
-    q.put((rank, _summary(rt), rt.stats.handoffs, max_inflight, rt.worker.steps))
+        for link in links.values():
+            link.phase = 1
+        q.put((rank, _summary(rt), rt.stats.handoffs, max_inflight, rt.stats.steps))
+    else:
+        ex = ReplicaExecutor(_host_worker(len(mine), MB), _params(MB), mine, seed=0,
+                             prefill_budget=2048)
+        srv = ReplicaServer(ex, links)
+        srv.serve_while(0)
+        assert all(not e.batch for e in ex.engines)
+        q.put((rank, [], 0, 0, ex.stats.steps))
     dist.barrier()
-    ch.close()
+    if rank == 0:
+        for link in links.values():
+            link.close()
+    else:
+        links.close()
     dist.destroy_process_group()
 
 
-def test_role_of():
-    assert role_of(0, 1) == (ROLE_BOTH, 0, -1)
-    assert role_of(0, 2) == (ROLE_GENERATOR, 0, 1)
-    assert role_of(1, 2) == (ROLE_FIXER, 0, 0)
-    assert role_of(5, 8) == (ROLE_FIXER, 1, 1)
-    assert role_of(2, 3)[0] == ROLE_BOTH
-
-
-def test_ring_roundtrip():
-    ch = PairChannel(f"cortex_test_{os.getpid()}", create=True, cap=4)
-    try:
-        for i in range(3):
-            ch.to_fixer.push(i, 0.5 * i)
-        assert ch.to_fixer.pop_all() == [(0, 0.0), (1, 0.5), (2, 1.0)]
-        assert ch.to_fixer.pop_all() == []
-        for i in range(4):  # wraps
-            ch.to_fixer.push(10 + i, 1.25)
-        with pytest.raises(RuntimeError):
-            ch.to_fixer.push(99, 0.0)
-        assert [r for r, _ in ch.to_fixer.pop_all()] == [10, 11, 12, 13]
-        ch.phase = 3
-        assert ch.phase == 3 and ch.to_generator.pop_all() == []
-    finally:
-        ch.close()
-
-
-def test_disjoint_pair_matches_single_rank():
-    rt = _runtime(ROLE_BOTH, None, 2)
-    rt.fill()
-    rt.run_until(N_WF, max_seconds=120)
-    want = _summary(rt)
+@pytest.mark.parametrize("mode,world,split", [("isolated", 2, None), ("isolated", 3, (1, 2)),
+                                              ("shared", 2, None), ("isolated", 4, (1, 3))])
+def test_pools_across_replicas_match_single_process(mode, world, split):
+    want = _single(mode)
     assert len(want) == N_WF
-
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_replica_proc, args=(r, world, port, mode, split, q))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = {}
     for _ in procs:
-        rank, summ, handoffs, inflight, steps = q.get(timeout=180)
+        rank, summ, handoffs, inflight, steps = q.get(timeout=240)
         res[rank] = (summ, handoffs, inflight, steps)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    gen, fix = res[0], res[1]
-    got = sorted(gen[0] + fix[0])
-    assert got == want
-    fixed = [s for s in want if any(st == FIXER for st, _ in s[2])]
-    assert gen[1] == len(fixed) == len(fix[0]) and fixed
-    assert gen[2] <= CONC
-    assert fix[3] > 0
+    summ, handoffs, inflight, _ = res[0]
+    assert summ == want
+    assert inflight <= CONC
+    assert handoffs > 0
+    # every replica's engines served calls (routing spreads each pool over its engines)
+    assert all(res[r][3] > 0 for r in range(world))
+    if mode == "isolated":
+        fixed = [s for s in want if any(st == FIXER for st, _ in s[2])]
+        assert fixed
