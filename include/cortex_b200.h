@@ -170,6 +170,34 @@ int32_t cortex_argmax(const float* logits, int64_t ld, int32_t n_rows, int32_t v
                       int32_t* out_tok, const int32_t* slot, int32_t* slot_tok, int32_t* hist,
                       int32_t hist_stride, const int32_t* hist_pos, cortex_stream_t stream);
 
+/* ---- fp32 decoder step (tiny config-1 model; storage and arithmetic fp32) ----
+ * Replaces the same EngineState transitions as the bf16 exports (admit -> prefill,
+ * advance_decode -> decode steps, stagesim/engines.py:142-194) when the engine is built
+ * with precision "f32": the north star's "1e-5 in fp32, greedy tokens identical" bar.
+ * cortex_f32_gemm: out[M, N] = X[M, K] W[N, K]^T; mode 0 plain, 1 + residual (out may
+ * alias it), 2 SwiGLU: W is [2N, K] (gate rows then up rows), out = silu(g) * u.
+ * cortex_f32_attention: per token t, causal attention over keys 0..tok_pos[t] of table
+ * row tok_row[t] (stage-prefix blocks for positions < tok_prefix[t], then private
+ * blocks); q / out [n_tok, hq, 128], KV cache rows of 128 fp32 (same layout as bf16). */
+int32_t cortex_f32_gemm(const float* x, int32_t ldx, const float* w, int32_t M, int32_t N,
+                        int32_t K, float* out, int32_t ldo, const float* residual, int32_t ldr,
+                        int32_t mode, cortex_stream_t stream);
+int32_t cortex_f32_embed(const float* emb, const int32_t* tokens, const int32_t* index,
+                         int32_t n_tok, int32_t d, float* out, cortex_stream_t stream);
+int32_t cortex_f32_rmsnorm(const float* x, const int32_t* rows, int32_t n_rows, const float* w,
+                           int32_t d, float eps, float* y, cortex_stream_t stream);
+int32_t cortex_f32_rope_kv_append(const float* qkv, float* q_out, float* cache, int64_t k_row0,
+                                  int64_t v_row0, const int32_t* table, int32_t table_stride,
+                                  const int32_t* tok_pos, const int32_t* tok_row,
+                                  const int32_t* tok_col, const int32_t* tok_off,
+                                  const float* cos_tab, const float* sin_tab, int32_t n_tok,
+                                  int32_t hq, int32_t hkv, cortex_stream_t stream);
+int32_t cortex_f32_attention(const float* q, const float* cache, int64_t k_row0, int64_t v_row0,
+                             const int32_t* table, int32_t table_stride, const int32_t* tok_row,
+                             const int32_t* tok_prefix, const int32_t* tok_pos, int32_t n_tok,
+                             int32_t hq, int32_t hkv, float scale, float* out,
+                             cortex_stream_t stream);
+
 /* Paged decode attention (one query token per sequence), split along the
  * context in fixed 512-token chunks + LSE combine. o_part/lse_part:
  * [n_seqs, max_splits, Hq, 128] / [n_seqs, max_splits, Hq] fp32 workspace.

@@ -48,20 +48,25 @@ def rope_tables(max_pos: int, theta: float) -> tuple[torch.Tensor, torch.Tensor]
             torch.from_numpy(np.sin(ang).astype(np.float32)))
 
 
-def rmsnorm_ref(h: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
+def no_round(x: torch.Tensor) -> torch.Tensor:
+    """No rounding (the fp32 path stores fp32)."""
+    return x
+
+
+def rmsnorm_ref(h: torch.Tensor, w: torch.Tensor, eps: float, rnd=bf16) -> torch.Tensor:
     rstd = torch.rsqrt((h * h).mean(dim=-1, keepdim=True) + eps)
-    return bf16(h * rstd * w)
+    return rnd(h * rstd * w)
 
 
-def rope_ref(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor:
+def rope_ref(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor, rnd=bf16) -> torch.Tensor:
     """x [T, H, 128] fp32 (bf16 values); cos/sin [T, 64]."""
     x0, x1 = x[..., :64], x[..., 64:]
     c, s = cos[:, None, :], sin[:, None, :]
-    return bf16(torch.cat([x0 * c - x1 * s, x1 * c + x0 * s], dim=-1))
+    return rnd(torch.cat([x0 * c - x1 * s, x1 * c + x0 * s], dim=-1))
 
 
 def attention_ref(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, q_pos: torch.Tensor,
-                  k_pos: torch.Tensor) -> torch.Tensor:
+                  k_pos: torch.Tensor, rnd=bf16) -> torch.Tensor:
     """Causal GQA attention in fp32. q [T, Hq, D], k/v [S, Hkv, D]; returns bf16-rounded [T, Hq, D]."""
     hq, hkv = q.shape[1], k.shape[1]
     group = hq // hkv
@@ -71,7 +76,7 @@ def attention_ref(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, q_pos: torc
     mask = k_pos[None, :] > q_pos[:, None]  # [T, S]
     s = s.masked_fill(mask[None], float("-inf"))
     p = torch.softmax(s, dim=-1)
-    return bf16(torch.einsum("hts,shd->thd", p, vv))
+    return rnd(torch.einsum("hts,shd->thd", p, vv))
 
 
 @dataclass(frozen=True)
@@ -87,10 +92,13 @@ class RefConfig:
 
 
 class RefDecoder:
-    """Weights as fp32 copies of the engine's bf16 tensors (exact)."""
+    """Weights as fp32 copies of the engine's tensors (exact). `exact=True`: no bf16
+    rounding anywhere (the oracle of the fp32 path, csrc/fp32.cu)."""
 
-    def __init__(self, cfg: RefConfig, weights: dict[str, torch.Tensor], max_pos: int) -> None:
+    def __init__(self, cfg: RefConfig, weights: dict[str, torch.Tensor], max_pos: int,
+                 exact: bool = False) -> None:
         self.cfg = cfg
+        self.rnd = no_round if exact else bf16
         self.w = {k: v.detach().to("cpu", torch.float32) for k, v in weights.items()}
         self.cos, self.sin = rope_tables(max_pos, cfg.rope_theta)
 
@@ -123,32 +131,33 @@ class RefSeq:
         n = toks.numel()
         pos = torch.arange(self.length, self.length + n)
         cos, sin = m.cos[pos], m.sin[pos]
+        rnd = m.rnd
         h = w["embed"][toks]
         hq, hkv = c.n_heads, c.n_kv_heads
         for li in range(c.n_layers):
             p = f"layers.{li}."
-            xn = rmsnorm_ref(h, w[p + "attn_norm"], c.eps)
-            qkv = bf16(xn @ w[p + "wqkv"].T)
+            xn = rmsnorm_ref(h, w[p + "attn_norm"], c.eps, rnd)
+            qkv = rnd(xn @ w[p + "wqkv"].T)
             q = qkv[:, : hq * HEAD_DIM].reshape(n, hq, HEAD_DIM)
             k = qkv[:, hq * HEAD_DIM:(hq + hkv) * HEAD_DIM].reshape(n, hkv, HEAD_DIM)
             v = qkv[:, (hq + hkv) * HEAD_DIM:].reshape(n, hkv, HEAD_DIM)
-            q = rope_ref(q, cos, sin)
-            k = rope_ref(k, cos, sin)
+            q = rope_ref(q, cos, sin, rnd)
+            k = rope_ref(k, cos, sin, rnd)
             self.k[li] = torch.cat([self.k[li], k])
             self.v[li] = torch.cat([self.v[li], v])
             kpos = torch.arange(self.k[li].shape[0])
-            a = attention_ref(q, self.k[li], self.v[li], pos, kpos).reshape(n, hq * HEAD_DIM)
+            a = attention_ref(q, self.k[li], self.v[li], pos, kpos, rnd).reshape(n, hq * HEAD_DIM)
             h = a @ w[p + "wo"].T + h
-            xn = rmsnorm_ref(h, w[p + "mlp_norm"], c.eps)
+            xn = rmsnorm_ref(h, w[p + "mlp_norm"], c.eps, rnd)
             gu = xn @ w[p + "wgu"].T  # fp32: SwiGLU is fused into the GEMM epilogue
             g, u = gu[:, : c.ffn], gu[:, c.ffn:]
-            act = bf16(g / (1.0 + torch.exp(-g)) * u)
+            act = rnd(g / (1.0 + torch.exp(-g)) * u)
             h = act @ w[p + "wd"].T + h
         self.length += n
         if want_logits == "none":
             return None
         hs = h if want_logits == "all" else h[-1:]
-        xn = rmsnorm_ref(hs, w["final_norm"], c.eps)
+        xn = rmsnorm_ref(hs, w["final_norm"], c.eps, rnd)
         return xn @ w["lm_head"].T
 
 

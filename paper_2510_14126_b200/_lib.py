@@ -64,6 +64,11 @@ SIGNATURES: dict[str, list] = {
                                P, P, I32, P],
     "cortex_paged_prefill_attn": [P, P, P, P, I32, P, P, P, P, P, I32, I32, I32, I32, I64, I64,
                                   F32, P],
+    "cortex_f32_gemm": [P, I32, P, I32, I32, I32, P, I32, P, I32, I32, P],
+    "cortex_f32_embed": [P, P, P, I32, I32, P, P],
+    "cortex_f32_rmsnorm": [P, P, I32, P, I32, F32, P, P],
+    "cortex_f32_rope_kv_append": [P, P, P, I64, I64, P, I32, P, P, P, P, P, P, I32, I32, I32, P],
+    "cortex_f32_attention": [P, P, I64, I64, P, I32, P, P, P, I32, I32, I32, F32, P, P],
     "cortex_sym_alloc": [U64, P],
     "cortex_sym_free": [P],
     "cortex_ipc_get_handle": [P, P],

@@ -57,6 +57,32 @@ def init_weights(cfg: ModelConfig, device, seed: int = 0, std: float = 0.02) -> 
     return w
 
 
+def init_weights_f32(cfg: ModelConfig, device, seed: int = 0, std: float = 0.02) -> dict:
+    """fp32 random-init weights for the fp32 path (config 1's exact-arithmetic check):
+    same distributions as init_weights, no bf16 rounding, canonical gate/up layout."""
+    g = torch.Generator(device=device).manual_seed(seed)
+
+    def rnd(*shape, s=std):
+        return torch.randn(*shape, generator=g, device=device) * s
+
+    def norm(d):
+        return 1.0 + 0.1 * torch.randn(d, generator=g, device=device)
+
+    d = cfg.d_model
+    w = {"embed": rnd(cfg.vocab, d, s=1.0)}
+    for i in range(cfg.n_layers):
+        p = f"layers.{i}."
+        w[p + "attn_norm"] = norm(d)
+        w[p + "wqkv"] = rnd(cfg.qkv_dim, d)
+        w[p + "wo"] = rnd(d, cfg.n_heads * HEAD_DIM)
+        w[p + "mlp_norm"] = norm(d)
+        w[p + "wgu"] = rnd(2 * cfg.ffn, d)
+        w[p + "wd"] = rnd(d, cfg.ffn)
+    w["final_norm"] = norm(d)
+    w["lm_head"] = rnd(cfg.vocab, d)
+    return w
+
+
 @dataclass
 class PrefillSeq:
     """New tokens of one sequence: positions [kv_len - n, kv_len) of table row `row`."""
@@ -144,9 +170,20 @@ class GpuWorker:
     def __init__(self, cfg: ModelConfig, device, n_blocks: int, n_rows: int, row_cols: int,
                  max_tokens: int = 4096, max_out: int = 512, hist_cols: int = 1024,
                  max_seq_tokens: int = 16384, weights: dict | None = None, seed: int = 0,
-                 tp=None) -> None:
+                 tp=None, precision: str = "bf16") -> None:
         # tp: a tp.TpComm when this worker is one rank of a TP = 2 replica. `cfg` is the
         # full model; the worker holds its rank's shard (tp.py) and self.cfg is the shard.
+        # precision "f32": every tensor and every kernel fp32 (csrc/fp32.cu) — the tiny
+        # config-1 model's exact-arithmetic path ("1e-5 in fp32, greedy tokens identical").
+        if precision not in ("bf16", "f32"):
+            raise ValueError(f"precision {precision!r}")
+        self.f32 = precision == "f32"
+        if self.f32:
+            if tp is not None:
+                raise ValueError("the fp32 path has no tensor parallelism")
+            self._init_f32(cfg, device, n_blocks, n_rows, row_cols, max_tokens, max_out,
+                           hist_cols, max_seq_tokens, weights, seed)
+            return
         self.full_cfg = cfg
         self.tp = tp
         if tp is not None:
@@ -245,10 +282,56 @@ class GpuWorker:
         self._ev_fork = torch.cuda.Event()
         self._ev_join = torch.cuda.Event()
 
+    def _init_f32(self, cfg, device, n_blocks, n_rows, row_cols, max_tokens, max_out, hist_cols,
+                  max_seq_tokens, weights, seed) -> None:
+        self.full_cfg = self.cfg = cfg
+        self.tp = None
+        self.device = dev = torch.device(device)
+        self.n_blocks, self.max_tokens, self.max_out = n_blocks, max_tokens, max_out
+        self.max_seq_tokens = max_seq_tokens
+        self.w = weights if weights is not None else init_weights_f32(cfg, dev, seed)
+        cos, sin = rope_tables(max_seq_tokens + 1, cfg.rope_theta)
+        self.cos = torch.from_numpy(cos).to(dev)
+        self.sin = torch.from_numpy(sin).to(dev)
+        f32 = torch.float32
+        self.cache = torch.zeros(cfg.n_layers, 2, n_blocks, cfg.n_kv_heads, BLOCK_TOKENS, HEAD_DIM,
+                                 dtype=f32, device=dev)
+        self.table = torch.zeros(n_rows, row_cols, dtype=torch.int32, device=dev)
+        self.slot_tok = torch.zeros(n_rows, dtype=torch.int32, device=dev)
+        self.hist = torch.zeros(n_rows, hist_cols, dtype=torch.int32, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        d, T = cfg.d_model, max_tokens
+        self.x = torch.zeros(T, d, dtype=f32, device=dev)
+        self.xn = torch.zeros(T, d, dtype=f32, device=dev)
+        self.qkv = torch.zeros(T, cfg.qkv_dim, dtype=f32, device=dev)
+        self.q = torch.zeros(T, cfg.n_heads * HEAD_DIM, dtype=f32, device=dev)
+        self.attn = torch.zeros(T, cfg.n_heads * HEAD_DIM, dtype=f32, device=dev)
+        self.act = torch.zeros(T, cfg.ffn, dtype=f32, device=dev)
+        self.xn_out = torch.zeros(max_out, d, dtype=f32, device=dev)
+        self.logits = torch.zeros(max_out, cfg.vocab, dtype=f32, device=dev)
+        self.out_tok = torch.zeros(max_out, dtype=torch.int32, device=dev)
+        self._meta_cap = 16 * (T + max_out) + 64
+        self._ring = 8
+        self.meta_host = [torch.zeros(self._meta_cap, dtype=torch.int32, pin_memory=True)
+                          for _ in range(self._ring)]
+        self.meta_evt = [None] * self._ring
+        self._meta_i = 0
+        self.meta_dev = torch.zeros(self._meta_cap, dtype=torch.int32, device=dev)
+        self.h2d_bytes = 0
+        self.scale = 1.0 / math.sqrt(HEAD_DIM)
+        self.launches = 0
+        self.steps = 0
+        self.on_forward = None
+        self.check_finite = False
+        self.tp_sync = None
+        self.prof = None
+
     # ------------------------------------------------------------------ helpers
 
     def oracle_weights(self) -> dict:
         """The weights in the canonical layout (gate rows then up rows) — for the checker."""
+        if self.f32:
+            return dict(self.w)
         out = dict(self.w)
         for i in range(self.cfg.n_layers):
             k = f"layers.{i}.wgu"
@@ -374,6 +457,9 @@ class GpuWorker:
             return
         if T > self.max_tokens:
             raise ValueError(f"step of {T} tokens exceeds max_tokens={self.max_tokens}")
+        if self.f32:
+            self._forward_f32(plan)
+            return
         i32 = np.int32
         pos = np.empty(T, i32)
         app_col = np.empty(T, i32)
@@ -608,6 +694,78 @@ class GpuWorker:
         if n_out:
             ops.rmsnorm(x, w["final_norm"], n_out, self.xn_out, cfg.eps, rows=d_orow)
             gemm("lm_head", self.xn_out_map, n_out, self.logits)
+            ops.argmax(self.logits, n_out, cfg.vocab, out_tok=self.out_tok, slot=d_oslot,
+                       slot_tok=self.slot_tok, hist=self.hist, hist_pos=d_ohist)
+            nl += 3
+        self.launches += nl
+        self.steps += 1
+        self.n_out = n_out
+        if self.on_forward is not None:
+            self.on_forward(plan, n_out)
+
+    def _forward_f32(self, plan: StepPlan) -> None:
+        """The fp32 step (csrc/fp32.cu): same plan semantics as the bf16 forward — decode
+        tokens first (input = slot_tok[row]), then prefill tokens — every tensor fp32."""
+        cfg, w = self.cfg, self.w
+        i32 = np.int32
+        n_dec, T = len(plan.decode), plan.n_tokens
+        pos, row, col, off, pre = (np.empty(T, i32) for _ in range(5))
+        tok_ids = np.zeros(T, i32)
+        out_rows, out_slot, out_hist = [], [], []
+        for i, d in enumerate(plan.decode):
+            p = d.kv_len - 1
+            c, o = token_slot(d.prefix_len, p)
+            pos[i], row[i], col[i], off[i], pre[i] = p, d.row, c, o, d.prefix_len
+            out_rows.append(i)
+            out_slot.append(d.row)
+            out_hist.append(d.hist_pos)
+        t = n_dec
+        for s in plan.prefill:
+            n = len(s.tokens)
+            for j, p in enumerate(range(s.kv_len - n, s.kv_len)):
+                if s.prefix_len and p < s.prefix_len:
+                    raise ValueError("prefill of a private segment cannot write prefix positions")
+                c, o = token_slot(s.prefix_len, p)
+                pos[t + j], row[t + j], col[t + j], off[t + j] = p, s.row, c, o
+            pre[t:t + n] = s.prefix_len
+            tok_ids[t:t + n] = s.tokens
+            if s.out_row >= 0:
+                out_rows.append(t + n - 1)
+                out_slot.append(s.out_row)
+                out_hist.append(s.hist_pos)
+            t += n
+        n_out = len(out_rows)
+        if n_out > self.max_out:
+            raise ValueError("too many output rows in one step")
+        (d_pos, d_row, d_col, d_off, d_pre, d_tok, d_orow, d_oslot, d_ohist) = self._upload([
+            pos, row, col, off, pre, tok_ids, np.asarray(out_rows, i32), np.asarray(out_slot, i32),
+            np.asarray(out_hist, i32)])
+        x, xn, hq, hkv = self.x, self.xn, cfg.n_heads, cfg.n_kv_heads
+        nl = 0
+        if n_dec:
+            ops.f32_embed(w["embed"], self.slot_tok, n_dec, x, index=d_row)
+            nl += 1
+        if T > n_dec:
+            ops.f32_embed(w["embed"], d_tok[n_dec:], T - n_dec, x[n_dec:])
+            nl += 1
+        plane = self.n_blocks * hkv * BLOCK_TOKENS
+        for li in range(cfg.n_layers):
+            p = f"layers.{li}."
+            k0, v0 = 2 * li * plane, (2 * li + 1) * plane
+            ops.f32_rmsnorm(x, w[p + "attn_norm"], T, xn, cfg.eps)
+            ops.f32_gemm(xn, T, w[p + "wqkv"], self.qkv)
+            ops.f32_rope_kv_append(self.qkv, self.q, self.cache, k0, v0, self.table, d_pos, d_row,
+                                   d_col, d_off, self.cos, self.sin, T, hq, hkv)
+            ops.f32_attention(self.q, self.cache, k0, v0, self.table, d_row, d_pre, d_pos, T, hq,
+                              hkv, self.scale, self.attn)
+            ops.f32_gemm(self.attn, T, w[p + "wo"], x, residual=x)
+            ops.f32_rmsnorm(x, w[p + "mlp_norm"], T, xn, cfg.eps)
+            ops.f32_gemm(xn, T, w[p + "wgu"], self.act, swiglu=True)
+            ops.f32_gemm(self.act, T, w[p + "wd"], x, residual=x)
+            nl += 8
+        if n_out:
+            ops.f32_rmsnorm(x, w["final_norm"], n_out, self.xn_out, cfg.eps, rows=d_orow)
+            ops.f32_gemm(self.xn_out, n_out, w["lm_head"], self.logits)
             ops.argmax(self.logits, n_out, cfg.vocab, out_tok=self.out_tok, slot=d_oslot,
                        slot_tok=self.slot_tok, hist=self.hist, hist_pos=d_ohist)
             nl += 3

@@ -357,3 +357,45 @@ def table_copy_h(table, src_rows, dst_rows, dst_cols, counts, stream=None) -> No
     _check(lib().cortex_table_copy_h(table.data_ptr(), table.stride(0), _hptr(s), _hptr(d),
                                      _hptr(k), _hptr(c), len(s), _stream(stream)),
            "cortex_table_copy_h")
+
+
+# ---------------------------------------------------------------- fp32 path (config 1)
+
+def f32_gemm(x: torch.Tensor, M: int, w: torch.Tensor, out: torch.Tensor,
+             residual: torch.Tensor | None = None, swiglu: bool = False, stream=None) -> None:
+    """out[:M] = x[:M] @ w^T (+ residual); swiglu: w = [gate; up] (2F x K), out [M, F]."""
+    N = w.shape[0] // 2 if swiglu else w.shape[0]
+    K = w.shape[1]
+    mode = 2 if swiglu else (1 if residual is not None else 0)
+    _check(lib().cortex_f32_gemm(x.data_ptr(), x.stride(0), w.data_ptr(), M, N, K,
+                                 out.data_ptr(), out.stride(0), _ptr(residual),
+                                 residual.stride(0) if residual is not None else 0, mode,
+                                 _stream(stream)), "cortex_f32_gemm")
+
+
+def f32_embed(emb, tokens, n_tok, out, index=None, stream=None) -> None:
+    _check(lib().cortex_f32_embed(emb.data_ptr(), tokens.data_ptr(), _ptr(index), n_tok,
+                                  emb.shape[1], out.data_ptr(), _stream(stream)),
+           "cortex_f32_embed")
+
+
+def f32_rmsnorm(x, w, n_rows, y, eps, rows=None, stream=None) -> None:
+    _check(lib().cortex_f32_rmsnorm(x.data_ptr(), _ptr(rows), n_rows, w.data_ptr(), x.shape[1],
+                                    eps, y.data_ptr(), _stream(stream)), "cortex_f32_rmsnorm")
+
+
+def f32_rope_kv_append(qkv, q_out, cache, k_row0, v_row0, table, tok_pos, tok_row, tok_col,
+                       tok_off, cos_tab, sin_tab, n_tok, hq, hkv, stream=None) -> None:
+    _check(lib().cortex_f32_rope_kv_append(
+        qkv.data_ptr(), q_out.data_ptr(), cache.data_ptr(), k_row0, v_row0, table.data_ptr(),
+        table.stride(0), tok_pos.data_ptr(), tok_row.data_ptr(), tok_col.data_ptr(),
+        tok_off.data_ptr(), cos_tab.data_ptr(), sin_tab.data_ptr(), n_tok, hq, hkv,
+        _stream(stream)), "cortex_f32_rope_kv_append")
+
+
+def f32_attention(q, cache, k_row0, v_row0, table, tok_row, tok_prefix, tok_pos, n_tok, hq, hkv,
+                  scale, out, stream=None) -> None:
+    _check(lib().cortex_f32_attention(
+        q.data_ptr(), cache.data_ptr(), k_row0, v_row0, table.data_ptr(), table.stride(0),
+        tok_row.data_ptr(), tok_prefix.data_ptr(), tok_pos.data_ptr(), n_tok, hq, hkv, scale,
+        out.data_ptr(), _stream(stream)), "cortex_f32_attention")
