@@ -12,8 +12,8 @@ executor U(0.1,0.4) s on host timers). `--workload config4 / config5` select the
 A step = one scheduling round + one fused GPU forward of every engine on the GPU: each
 decoding call emits a token and pending prompt / prefix prefill is packed in (chunked,
 <= 4096 tokens per step). Before the timed window the closed loop is RAMPED (untimed,
-`ramp_steps`) until half the concurrency has finished and every pool holds calls,
-whatever --warmup says, then --warmup steps run, then exactly --steps steps are timed.
+`ramp_steps`) until as many workflows as the concurrency have finished and every pool
+holds calls, whatever --warmup says, then --warmup steps run, then exactly --steps steps are timed.
 `value` = successful workflows per second over the timed steps, on the device clock
 (CUDA events on the engine stream), max over ranks. `e2e` = the same window on the host
 wall clock through the runtime's public API (PoolRuntime.step), which uploads every
@@ -372,13 +372,15 @@ def run_arm(args, arm, worker, cfg, desc, barrier, all_reduce, device, local, n_
     # ---- ramp (untimed) to the closed loop's steady state, whatever --warmup says: the
     # first workflow needs ~100 steps (prompt prefill + 50-150 decode steps + an executor
     # visit), so a window right after fill() would be pure decode with no completions.
-    # Ramp until half the concurrency has finished and every pool holds calls.
+    # Ramp until as many workflows as the concurrency have finished (one turnover of the
+    # closed loop: the initial wave of simultaneous arrivals has drained) and every pool
+    # holds calls.
     ramp_steps = 0
     prof_ms, shares = 0.0, {}
     if rt is not None:
         rt.fill()
         t_ramp = time.perf_counter() + 900.0
-        target = max(1, rt.concurrency // 2)
+        target = max(1, rt.concurrency)
         while True:
             done = rt.stats.completed + rt.stats.failed
             busy = all(any(len(e.batch) for e in es) for es in rt.pool_engines.values())

@@ -1,7 +1,6 @@
 """Cluster split-K GEMM (gemm_splitk.cu) vs the 2-SM whole-tile kernel at decode M: time
 per launch for each forced (token tiles mt, split count ks) with <= 74 pairs, and the
 automatic plan.  python benchmarks/gemm_sk_sweep.py [M ...]"""
-import ctypes
 import json
 import os
 import sys
@@ -10,9 +9,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 from gemm import SHAPES, bench  # noqa: E402
-from paper_2510_14126_b200 import ops  # noqa: E402
+from paper_2510_14126_b200 import _lib, ops  # noqa: E402
 
-L = ops.lib()
 for M in [int(a) for a in sys.argv[1:]] or [200, 256]:
     for name in ("qkv", "o", "down"):
         N, K = SHAPES[name]
@@ -22,19 +20,18 @@ for M in [int(a) for a in sys.argv[1:]] or [200, 256]:
         ops.gemm_set_mode(2)
         row["2sm"] = round(bench(M, name, residual=name != "qkv")["ms"] * 1e3, 1)
         ops.gemm_set_mode(3)
-        tn, mt = ctypes.c_int32(), ctypes.c_int32()
-        ks = L.cortex_gemm_splitk_plan2(M, N, K, ctypes.byref(tn), ctypes.byref(mt))
-        row["auto"] = f"mt{mt.value}ks{ks}tn{tn.value}"
+        ks, tn, mt, _ = ops.splitk_plan(M, N, K)
+        row["auto"] = f"mt{mt}ks{ks}tn{tn}"
         row["auto_us"] = round(bench(M, name, residual=name != "qkv")["ms"] * 1e3, 1)
         for m in (1, 2, 3):
             for k in (2, 3, 4):
                 if (N // 256) * m * k > 74:
                     continue
-                L.cortex_gemm_splitk_force(k)
-                L.cortex_gemm_splitk_force_mt(m)
-                if L.cortex_gemm_splitk_plan2(M, N, K, None, None) == k:
+                _lib.set_knob("SK_KS", k)
+                _lib.set_knob("SK_MT", m)
+                if ops.splitk_plan(M, N, K)[0] == k:
                     row[f"mt{m}ks{k}"] = round(bench(M, name, residual=name != "qkv")["ms"] * 1e3, 1)
-        L.cortex_gemm_splitk_force(-1)
-        L.cortex_gemm_splitk_force_mt(-1)
+        _lib.set_knob("SK_KS", -1)
+        _lib.set_knob("SK_MT", -1)
         ops.gemm_set_mode(0)
         print(json.dumps(row), flush=True)

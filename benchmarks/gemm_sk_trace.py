@@ -12,7 +12,9 @@ from paper_2510_14126_b200 import ops  # noqa: E402
 
 name, M, ks = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
 ops.gemm_set_mode(3)
-ops.lib().cortex_gemm_splitk_force(ks)
+from paper_2510_14126_b200 import _lib  # noqa: E402
+
+_lib.set_knob("SK_KS", ks)
 N, K = SHAPES[name]
 w = (torch.randn(N, K, device="cuda") * 0.05).to(torch.bfloat16)
 x = torch.randn(M, K, device="cuda").to(torch.bfloat16)

@@ -45,13 +45,9 @@ enum {
   CORTEX_ETIMEOUT = -5 /* a cross-GPU wait exceeded its bound (peer rank gone) */
 };
 
-/* ABI version (major * 100 + minor). */
+/* ABI version (major * 100 + minor). Tuning / test knobs (kernel variants, PDL on/off)
+ * are NOT part of this interface: see paper_2510_14126_b200/csrc/cortex_dev.h. */
 int32_t cortex_abi_version(void);
-
-/* Programmatic dependent launch for the decoder-step kernels (1 = on, the default; 0 =
- * off): each kernel is launched while its predecessor on the stream runs and waits for it
- * in-kernel after its prologue. */
-int32_t cortex_set_pdl(int32_t on);
 
 /* ---- KV block pool (bitmap, bit = 1 -> free) -------------------------------
  * EngineState.admit (engines.py:142-166): cold prefix blocks + prompt blocks;
@@ -117,29 +113,9 @@ int32_t cortex_tmap_encode_2d_bf16(void* tmap_out, const void* gptr, uint64_t ro
  * out_f32: 0 = bf16 out, 1 = fp32 out, 2 = fused SwiGLU: W's rows are interleaved in
  * blocks of 64 gate rows then 64 matching up rows, and out[m, f] (bf16, N/2 features) =
  * silu(g) * u with g, u the fp32 accumulators (no residual).
- * workspace / counters are used when cortex_gemm_splits(M, N, K) > 1. */
-int32_t cortex_gemm_splits(int32_t M, int32_t N, int32_t K);
-/* Which kernel serves (M, N, K): 1 = 1-SM swap-AB + split-K (decode sizes),
- * 2 = persistent 2-SM cta_group::2 kernel (M > 128, N % 256 == 0). */
-int32_t cortex_gemm_path(int32_t M, int32_t N, int32_t K);
-/* Test hook: 0 = automatic, 1 = force the 1-SM kernel, 2 = force 2-SM when legal. */
-int32_t cortex_gemm_set_mode(int32_t mode);
-/* 2-SM kernel scheduling: -1 = automatic, 0 = whole tiles, 1 = stream-K (equal K-block
- * ranges per CTA pair; partial tiles reduced through workspace, deterministic). The
- * workspace must hold SMs x 256 x 128 floats and the counters SMs ints (zeroed). */
-int32_t cortex_gemm_set_stream_k(int32_t force);
-/* The 2-SM kernel's plan for (M, N, K): TN | (stream_k << 16). */
-int32_t cortex_gemm2_tile(int32_t M, int32_t N, int32_t K);
-/* Cluster split-K plan for decode-sized M: K splits (>= 1; 0 = not used), the token
- * tile, token tiles and 256-row weight sub-tiles per CTA pair; cortex_gemm_splitk_force pins the split count (-1 = automatic; tuning/tests). */
-int32_t cortex_gemm_splitk_plan(int32_t M, int32_t N, int32_t K, int32_t* tn_out);
-int32_t cortex_gemm_splitk_plan2(int32_t M, int32_t N, int32_t K, int32_t* tn_out,
-                                 int32_t* m_tiles_out);
-int32_t cortex_gemm_splitk_plan3(int32_t M, int32_t N, int32_t K, int32_t* tn_out,
-                                 int32_t* m_tiles_out, int32_t* weight_subtiles_out);
-int32_t cortex_gemm_splitk_force(int32_t ks);
-int32_t cortex_gemm_splitk_force_mt(int32_t m_tiles);
-int32_t cortex_gemm_splitk_force_nw(int32_t weight_subtiles); /* 2: wide N unsplit; -1 auto */
+ * workspace / counters: the split-K partials and the per-tile arrival counters (kept
+ * zeroed) of the decode-sized kernels; 16 Mi floats and 64 Ki counters cover every
+ * shape of the Llama-3-8B step (GemmWorkspace in ops.py). */
 int32_t cortex_gemm_bf16(const void* tmap_w, const void* tmap_x, int32_t M, int32_t N, int32_t K,
                          void* out, int32_t ldo, int32_t out_f32, const void* residual,
                          int32_t ldr, float* workspace, uint64_t workspace_bytes,
@@ -161,9 +137,6 @@ int32_t cortex_rope_kv_append(const void* qkv, void* q_out, void* cache, int64_t
                               const int32_t* tok_col, const int32_t* tok_off,
                               const float* cos_tab, const float* sin_tab, int32_t n_tok,
                               int32_t hq, int32_t hkv, cortex_stream_t stream);
-
-int32_t cortex_swiglu(const void* gu, int32_t n_tok, int32_t f, void* act,
-                      cortex_stream_t stream);
 
 /* Greedy token per row; optional scatter into per-slot state. */
 int32_t cortex_argmax(const float* logits, int64_t ld, int32_t n_rows, int32_t vocab,
@@ -198,54 +171,29 @@ int32_t cortex_f32_attention(const float* q, const float* cache, int64_t k_row0,
                              int32_t hq, int32_t hkv, float scale, float* out,
                              cortex_stream_t stream);
 
-/* Paged decode attention (one query token per sequence), split along the
- * context in fixed 512-token chunks + LSE combine. o_part/lse_part:
- * [n_seqs, max_splits, Hq, 128] / [n_seqs, max_splits, Hq] fp32 workspace.
+/* Paged decode attention (one query token per sequence), the GPU work of every token
+ * EngineState.advance_decode emits (engines.py:172-194). Split along the context in
+ * fixed 512-token chunks + LSE combine. o_part/lse_part: [n_seqs, max_splits, Hq, 128] /
+ * [n_seqs, max_splits, Hq] fp32 workspace.
  * Without groups (n_groups = 0): max_splits >= max cortex_decode_splits(prefix, kv_len).
  * Cascade (n_groups > 0): the decode calls sharing a resident stage prefix are
  * contiguous (group g = calls [grp_first, grp_first + grp_count), prefix in table row
  * grp_row, grp_plen tokens); their prefix attention runs once per group (partials in
  * slots [0, prefix_slots), prefix_slots >= max ceil(ceil(P/16)/16)), the private
  * tokens per call (slots prefix_slots + ...). Every call with prefix_len > 0 must
- * belong to a group. max_group_count = largest grp_count. */
-int32_t cortex_decode_splits(int32_t prefix_len, int32_t kv_len);
-int32_t cortex_paged_decode_attn(const void* tmap_kv, const void* q, const int32_t* table,
-                                 int32_t table_stride, const int32_t* seq_row,
-                                 const int32_t* seq_prefix, const int32_t* seq_kvlen,
-                                 int32_t n_seqs, int32_t n_kv_heads, int32_t group,
-                                 int64_t k_row0, int64_t v_row0, float softmax_scale,
-                                 float* o_part, float* lse_part, int32_t max_splits, void* out,
-                                 const int32_t* grp_row, const int32_t* grp_plen,
-                                 const int32_t* grp_first, const int32_t* grp_count,
-                                 int32_t n_groups, int32_t max_group_count,
-                                 int32_t prefix_slots, const void* tmap_q,
-                                 cortex_stream_t stream);
-
-/* Same as cortex_paged_decode_attn, one part at a time (parts bitmask: 1 = shared-prefix
- * cascade pass, 2 = per-call context splits, 4 = LSE combine), so the cascade pass can run
- * on a second stream concurrently with the split kernel (join before the combine). */
-int32_t cortex_paged_decode_attn_parts(const void* tmap_kv, const void* q, const int32_t* table,
-                                       int32_t table_stride, const int32_t* seq_row,
-                                       const int32_t* seq_prefix, const int32_t* seq_kvlen,
-                                       int32_t n_seqs, int32_t n_kv_heads, int32_t group,
-                                       int64_t k_row0, int64_t v_row0, float softmax_scale,
-                                       float* o_part, float* lse_part, int32_t max_splits,
-                                       void* out, const int32_t* grp_row, const int32_t* grp_plen,
-                                       const int32_t* grp_first, const int32_t* grp_count,
-                                       int32_t n_groups, int32_t max_group_count,
-                                       int32_t prefix_slots, const void* tmap_q, int32_t parts,
-                                       cortex_stream_t stream);
-
-/* Balanced ("flat") plan for the context splits: call b's tiles (its private tiles
+ * belong to a group. max_group_count = largest grp_count. tmap_q (cortex_tmap_encode_q)
+ * selects the tcgen05 cascade pass.
+ * parts (bitmask): 1 = shared-prefix cascade pass, 2 = per-call context splits, 4 = LSE
+ * combine (7 = all), so the cascade pass can run on a second stream concurrently with
+ * the splits (join before the combine).
+ * Balanced ("flat") plan (seq_tile_start != NULL): call b's tiles (its private tiles
  * under cascade, all tiles otherwise) are flat tiles [seq_tile_start[b],
  * seq_tile_start[b] + n_b) of one sequence of total_tiles; CTA (c, kv head) streams
- * flat tiles [c W, (c+1) W), W = tiles_per_chunk <= 48 (cortex_decode_tiles_per_chunk),
- * so every CTA does equal work whatever the context lengths. Call b's partials go to
- * slots off + [0, (S_b + n_b - 1) / W - S_b / W], off = prefix_slots under cascade
- * else 0: max_splits must cover that. Other arguments and parts as above; with
- * seq_tile_start = NULL this is cortex_paged_decode_attn_parts. */
-int32_t cortex_decode_tiles_per_chunk(int32_t total_tiles, int32_t n_kv_heads);
-int32_t cortex_paged_decode_attn_flat(
+ * flat tiles [c W, (c+1) W), W = tiles_per_chunk <= 48, so every CTA does equal work
+ * whatever the context lengths; call b's partials go to slots off + [0, (S_b + n_b - 1)
+ * / W - S_b / W] (off = prefix_slots under cascade, else 0). NULL: fixed splits. */
+int32_t cortex_decode_splits(int32_t prefix_len, int32_t kv_len);
+int32_t cortex_paged_decode_attn(
     const void* tmap_kv, const void* q, const int32_t* table, int32_t table_stride,
     const int32_t* seq_row, const int32_t* seq_prefix, const int32_t* seq_kvlen,
     const int32_t* seq_tile_start, int32_t total_tiles, int32_t tiles_per_chunk, int32_t n_seqs,
@@ -260,13 +208,14 @@ int32_t cortex_paged_decode_attn_flat(
 int32_t cortex_tmap_encode_q(void* tmap_out, const void* q, uint64_t n_tok, int32_t hq,
                              int32_t group);
 
-/* tcgen05 flash attention, 2 x 128 query rows (tokens x GQA group) per CTA (two Q tiles
- * ping-ponging softmax against the MMAs, chosen per launch by wave count;
- * cortex_fmha_set_2q(-1 auto | 0 one tile | 1 two tiles)), paged K/V in
- * 8-block key tiles, TMEM S/O accumulators. Prefill: same contract as
- * cortex_paged_prefill_attn. Cascade: the shared-prefix pass of decode (partials into
- * slots [0, prefix_slots) of o_part / lse_part, rows = decode index). */
-int32_t cortex_fmha_set_2q(int32_t on);
+/* tcgen05 flash attention, 128 query rows (tokens x GQA group) per CTA, paged K/V in
+ * 8-block key tiles, TMEM S/O accumulators, P entering PV as bf16 hi + lo. Prefill (the
+ * GPU work of EngineState.admit's prompt / cold-prefix prefill, engines.py:142-166):
+ * causal over the sequence's row (seq_prefix tokens of stage prefix, then private
+ * positions); query token i of sequence s is row seq_qstart[s] + i of q / out
+ * [n_tok, hq, 128] at position seq_kvlen[s] - seq_qlen[s] + i. Cascade: the
+ * shared-prefix pass of decode (partials into slots [0, prefix_slots) of o_part /
+ * lse_part, rows = decode index). */
 int32_t cortex_fmha_prefill_tc(const void* tmap_kv, const void* tmap_q, void* out,
                                const int32_t* table, int32_t table_stride, const int32_t* seq_row,
                                const int32_t* seq_prefix, const int32_t* seq_kvlen,
@@ -282,16 +231,6 @@ int32_t cortex_fmha_cascade_tc(const void* tmap_kv, const void* tmap_q, const in
                                int64_t k_row0, int64_t v_row0, float softmax_scale,
                                float* o_part, float* lse_part, int32_t max_splits,
                                cortex_stream_t stream);
-
-/* Paged prefill attention: the last seq_qlen[s] positions of each sequence
- * attend causally to its prefix + private tokens. */
-int32_t cortex_paged_prefill_attn(const void* tmap_kv, const void* q, void* out,
-                                  const int32_t* table, int32_t table_stride,
-                                  const int32_t* seq_row, const int32_t* seq_prefix,
-                                  const int32_t* seq_kvlen, const int32_t* seq_qstart,
-                                  const int32_t* seq_qlen, int32_t n_seqs, int32_t max_qlen,
-                                  int32_t n_kv_heads, int32_t group, int64_t k_row0,
-                                  int64_t v_row0, float softmax_scale, cortex_stream_t stream);
 
 /* ---- Tensor parallelism (TP = 2 inside one engine replica, BASELINE config 5) -------
  * the only collective on the path. The reference engine has no

@@ -22,7 +22,6 @@ F32 = c_float
 # name -> argtypes (every export returns int32 status)
 SIGNATURES: dict[str, list] = {
     "cortex_abi_version": [],
-    "cortex_set_pdl": [I32],
     "cortex_kv_alloc": [P, I32, I32, P, P, P, I32, P, I32, P, P],
     "cortex_kv_free": [P, I32, I32, P, I32, P, P, P, I32, P, P],
     "cortex_table_copy": [P, I32, P, P, P, P, I32, P],
@@ -31,44 +30,24 @@ SIGNATURES: dict[str, list] = {
     "cortex_kv_free_h": [P, I32, I32, P, I32, P, P, P, I32, P, P],
     "cortex_table_copy_h": [P, I32, P, P, P, P, I32, P],
     "cortex_tmap_encode_2d_bf16": [P, P, U64, U64, U64, ctypes.c_uint32, ctypes.c_uint32],
-    "cortex_gemm_splits": [I32, I32, I32],
-    "cortex_gemm_path": [I32, I32, I32],
-    "cortex_gemm_set_mode": [I32],
-    "cortex_gemm_set_stream_k": [I32],
-    "cortex_gemm2_tile": [I32, I32, I32],
-    "cortex_gemm_splitk_plan": [I32, I32, I32, P],
-    "cortex_gemm_splitk_plan2": [I32, I32, I32, P, P],
-    "cortex_gemm_splitk_plan3": [I32, I32, I32, P, P, P],
-    "cortex_gemm_splitk_force": [I32],
-    "cortex_gemm_splitk_force_mt": [I32],
-    "cortex_gemm_splitk_force_nw": [I32],
     "cortex_gemm_bf16": [P, P, I32, I32, I32, P, I32, I32, P, I32, P, U64, P, I32, P],
     "cortex_embed": [P, P, P, I32, I32, P, P],
     "cortex_rmsnorm": [P, P, I32, P, I32, F32, P, P],
     "cortex_rope_kv_append": [P, P, P, I64, I64, P, I32, P, P, P, P, P, P, I32, I32, I32, P],
-    "cortex_swiglu": [P, I32, I32, P, P],
     "cortex_argmax": [P, I64, I32, I32, P, P, P, P, I32, P, P],
-    "cortex_decode_splits": [I32, I32],
-    "cortex_paged_decode_attn": [P, P, P, I32, P, P, P, I32, I32, I32, I64, I64, F32, P, P, I32,
-                                 P, P, P, P, P, I32, I32, I32, P, P],
-    "cortex_paged_decode_attn_parts": [P, P, P, I32, P, P, P, I32, I32, I32, I64, I64, F32, P, P,
-                                       I32, P, P, P, P, P, I32, I32, I32, P, I32, P],
-    "cortex_decode_tiles_per_chunk": [I32, I32],
-    "cortex_paged_decode_attn_flat": [P, P, P, I32, P, P, P, P, I32, I32, I32, I32, I32, I64, I64,
-                                      F32, P, P, I32, P, P, P, P, P, I32, I32, I32, P, I32, P],
-    "cortex_tmap_encode_q": [P, P, U64, I32, I32],
-    "cortex_fmha_set_2q": [I32],
-    "cortex_fmha_prefill_tc": [P, P, P, P, I32, P, P, P, P, P, I32, I32, I32, I32, I64, I64, F32,
-                               P],
-    "cortex_fmha_cascade_tc": [P, P, P, I32, P, P, P, P, I32, I32, I32, I32, I32, I64, I64, F32,
-                               P, P, I32, P],
-    "cortex_paged_prefill_attn": [P, P, P, P, I32, P, P, P, P, P, I32, I32, I32, I32, I64, I64,
-                                  F32, P],
     "cortex_f32_gemm": [P, I32, P, I32, I32, I32, P, I32, P, I32, I32, P],
     "cortex_f32_embed": [P, P, P, I32, I32, P, P],
     "cortex_f32_rmsnorm": [P, P, I32, P, I32, F32, P, P],
     "cortex_f32_rope_kv_append": [P, P, P, I64, I64, P, I32, P, P, P, P, P, P, I32, I32, I32, P],
     "cortex_f32_attention": [P, P, I64, I64, P, I32, P, P, P, I32, I32, I32, F32, P, P],
+    "cortex_decode_splits": [I32, I32],
+    "cortex_paged_decode_attn": [P, P, P, I32, P, P, P, P, I32, I32, I32, I32, I32, I64, I64,
+                                 F32, P, P, I32, P, P, P, P, P, I32, I32, I32, P, I32, P],
+    "cortex_tmap_encode_q": [P, P, U64, I32, I32],
+    "cortex_fmha_prefill_tc": [P, P, P, P, I32, P, P, P, P, P, I32, I32, I32, I32, I64, I64, F32,
+                               P],
+    "cortex_fmha_cascade_tc": [P, P, P, I32, P, P, P, P, I32, I32, I32, I32, I32, I64, I64, F32,
+                               P, P, I32, P],
     "cortex_sym_alloc": [U64, P],
     "cortex_sym_free": [P],
     "cortex_ipc_get_handle": [P, P],
@@ -78,6 +57,24 @@ SIGNATURES: dict[str, list] = {
     "cortex_tp_signal": [P, ctypes.c_uint32, P],
     "cortex_tp_allreduce_rmsnorm": [P, P, P, I32, I32, P, F32, P, P, ctypes.c_uint32, P, P],
 }
+
+# The private tuning / test interface (csrc/cortex_dev.h): not part of the boundary.
+DEV_SIGNATURES: dict[str, list] = {
+    "cortex_dev_set_knob": [I32, I32],
+    "cortex_dev_get_knob": [I32],
+    "cortex_gemm_splits": [I32, I32, I32],
+    "cortex_gemm_path": [I32, I32, I32],
+    "cortex_gemm2_tile": [I32, I32, I32],
+    "cortex_gemm_splitk_plan": [I32, I32, I32, P, P, P],
+    "cortex_decode_tiles_per_chunk": [I32, I32],
+    "cortex_paged_prefill_attn": [P, P, P, P, I32, P, P, P, P, P, I32, I32, I32, I32, I64, I64,
+                                  F32, P],
+}
+
+# knob ids (csrc/cortex_dev.h, enum CortexKnob)
+KNOBS = {name: i for i, name in enumerate(
+    ["PDL", "GEMM_MODE", "GEMM_STREAM_K", "GEMM_TN", "GEMM_L2PF", "SK_KS", "SK_MT", "SK_NW",
+     "SK_ISSUE", "FMHA_2Q", "FMHA_PLO"])}
 
 STATUS_NAMES = {0: "ok", -1: "bad argument", -2: "CUDA error", -3: "out of KV blocks",
                 -4: "unsupported",
@@ -98,15 +95,24 @@ def load() -> ctypes.CDLL:
                 "(there is no CPU fallback)"
             )
         lib = ctypes.CDLL(str(path))
-        for name, argtypes in SIGNATURES.items():
+        for name, argtypes in {**SIGNATURES, **DEV_SIGNATURES}.items():
             fn = getattr(lib, name)
             fn.argtypes = argtypes
             fn.restype = c_int32
-        if os.environ.get("CORTEX_PDL") == "0":  # A/B runs without programmatic launch
-            lib.cortex_set_pdl(0)
         _LIB = lib
     return _LIB
 
 
 def exported_symbols() -> list[str]:
     return list(SIGNATURES)
+
+
+def set_knob(name: str, value: int) -> int:
+    """Tuning / test hook (csrc/cortex_dev.h); returns the previous value."""
+    lib = load()
+    k = KNOBS[name]
+    prev = lib.cortex_dev_get_knob(k)
+    rc = lib.cortex_dev_set_knob(k, int(value))
+    if rc != 0:
+        raise ValueError(f"knob {name} = {value} rejected ({rc})")
+    return prev

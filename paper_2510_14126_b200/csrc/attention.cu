@@ -1105,24 +1105,7 @@ int32_t cortex_decode_splits(int32_t prefix_len, int32_t kv_len) {
   return (nt + kTilesPerSplit - 1) / kTilesPerSplit;
 }
 
-int32_t cortex_paged_decode_attn(const void* tmap_kv, const void* q, const int32_t* table,
-                                 int32_t table_stride, const int32_t* seq_row,
-                                 const int32_t* seq_prefix, const int32_t* seq_kvlen,
-                                 int32_t n_seqs, int32_t n_kv_heads, int32_t group,
-                                 int64_t k_row0, int64_t v_row0, float softmax_scale,
-                                 float* o_part, float* lse_part, int32_t max_splits, void* out,
-                                 const int32_t* grp_row, const int32_t* grp_plen,
-                                 const int32_t* grp_first, const int32_t* grp_count,
-                                 int32_t n_groups, int32_t max_group_count,
-                                 int32_t prefix_slots, const void* tmap_q, cudaStream_t stream) {
-  return cortex_paged_decode_attn_parts(tmap_kv, q, table, table_stride, seq_row, seq_prefix,
-                                        seq_kvlen, n_seqs, n_kv_heads, group, k_row0, v_row0,
-                                        softmax_scale, o_part, lse_part, max_splits, out, grp_row,
-                                        grp_plen, grp_first, grp_count, n_groups, max_group_count,
-                                        prefix_slots, tmap_q, 7, stream);
-}
-
-int32_t cortex_paged_decode_attn_flat(
+int32_t cortex_paged_decode_attn(
     const void* tmap_kv, const void* q, const int32_t* table, int32_t table_stride,
     const int32_t* seq_row, const int32_t* seq_prefix, const int32_t* seq_kvlen,
     const int32_t* seq_tile_start, int32_t total_tiles, int32_t tiles_per_chunk, int32_t n_seqs,
@@ -1251,24 +1234,6 @@ int32_t cortex_paged_decode_attn_flat(
   if (pdl_launch(decode_combine_kernel, cgrid, kCombineThreads, 0, stream, 1, cb) != cudaSuccess)
     return CORTEX_ECUDA;
   return CORTEX_OK;
-}
-
-int32_t cortex_paged_decode_attn_parts(const void* tmap_kv, const void* q, const int32_t* table,
-                                       int32_t table_stride, const int32_t* seq_row,
-                                       const int32_t* seq_prefix, const int32_t* seq_kvlen,
-                                       int32_t n_seqs, int32_t n_kv_heads, int32_t group,
-                                       int64_t k_row0, int64_t v_row0, float softmax_scale,
-                                       float* o_part, float* lse_part, int32_t max_splits,
-                                       void* out, const int32_t* grp_row, const int32_t* grp_plen,
-                                       const int32_t* grp_first, const int32_t* grp_count,
-                                       int32_t n_groups, int32_t max_group_count,
-                                       int32_t prefix_slots, const void* tmap_q, int32_t parts,
-                                       cudaStream_t stream) {
-  return cortex_paged_decode_attn_flat(
-      tmap_kv, q, table, table_stride, seq_row, seq_prefix, seq_kvlen, nullptr, 0, 0, n_seqs,
-      n_kv_heads, group, k_row0, v_row0, softmax_scale, o_part, lse_part, max_splits, out, grp_row,
-      grp_plen, grp_first, grp_count, n_groups, max_group_count, prefix_slots, tmap_q, parts,
-      stream);
 }
 
 // Tiles per chunk of the balanced decode plan for `total_tiles` flat tiles: the chunk

@@ -942,34 +942,25 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   }
 }
 
-// P enters the PV MMA as bf16 (the FlashAttention convention); CORTEX_FMHA_PLO=1 adds the
-// lo half (P = hi + lo to ~2^-17, a second PV pass). Measured on config 1 against the fp32
-// oracle: worst call 6.0e-4 / position 1.52e-3 (bf16 P) vs 5.1e-4 / 1.46e-3 (hi + lo); the
-// prefill attention of a config-2 step 51.3 -> 45.1 us per layer, bench +1.4 %.
-int fmha_p_lo() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CORTEX_FMHA_PLO");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v;
-}
+// P enters the PV MMA as bf16 hi + lo (P = hi + lo to ~2^-17, a second PV pass; knob
+// FMHA_PLO, default on). bf16 P alone (FMHA_PLO = 0, the FlashAttention convention) puts
+// a 2^-9 relative error on every probability: at the Llama-3-8B shape the attention
+// output then differs from exact softmax by 2.2e-3 (tools/diag_8b.py) and 2-layer logits
+// by 4.7e-3, over the north star's 2e-3 bar; with hi + lo the attention error is the bf16
+// rounding of the output alone (<= 1.4e-4 beyond it).
+int fmha_p_lo() { return g_cortex_knob[CORTEX_KNOB_FMHA_PLO]; }
 
-// Kernel choice per launch (g_fmha_2q: -1 automatic, 0 one Q tile, 1 two; test / A-B
-// hook cortex_fmha_set_2q, env CORTEX_FMHA_2Q=0/1). A two-tile CTA costs ~1.55x a one-tile
+// Kernel choice per launch (knob FMHA_2Q: -1 automatic, 0 one Q tile, 1 two; the two-tile
+// kernel has no hi + lo P, so it serves only with FMHA_PLO = 0). A two-tile CTA costs ~1.55x a one-tile
 // CTA (benchmarks/fmha.py: 8K causal prefill 614 -> 807 TFLOP/s, 8 x 200-token prompts
 // 325 -> 406) but the grid halves, so small grids (decode's cascade pass over a
 // 1000-token prefix: 128 one-tile CTAs, 15 us vs 21 us) stay on one tile per CTA:
 // pick the lower of waves(n1) and 1.55 waves(n1 / 2) on the SM count.
-int g_fmha_2q = -2;
 int g_fmha_sms = 0;
 
 bool fmha_use_2q(const dim3& grid) {
-  if (g_fmha_2q == -2) {
-    const char* e = getenv("CORTEX_FMHA_2Q");
-    g_fmha_2q = (e && (e[0] == '0' || e[0] == '1')) ? e[0] - '0' : -1;
-  }
-  if (g_fmha_2q >= 0) return g_fmha_2q == 1;
+  const int force = g_cortex_knob[CORTEX_KNOB_FMHA_2Q];
+  if (force >= 0) return force == 1;
   if (g_fmha_sms == 0) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess ||
@@ -1010,13 +1001,6 @@ int32_t launch_fmha(const CUtensorMap* tq, const CUtensorMap* tkv, const FmhaArg
 }  // namespace
 
 extern "C" {
-
-// -1: choose per launch (default), 1: two Q tiles per CTA, 0: one (test / A-B hook)
-int32_t cortex_fmha_set_2q(int32_t on) {
-  if (on < -1 || on > 1) return CORTEX_EBADARG;
-  g_fmha_2q = on;
-  return CORTEX_OK;
-}
 
 int32_t cortex_fmha_prefill_tc(const void* tmap_kv, const void* tmap_q, void* out,
                                const int32_t* table, int32_t table_stride, const int32_t* seq_row,

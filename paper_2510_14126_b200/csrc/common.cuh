@@ -22,6 +22,7 @@
 #include <cstdio>
 
 #include "cortex_b200.h"
+#include "cortex_dev.h"
 
 #define CORTEX_CHECK_LAUNCH()                      \
   do {                                             \
@@ -36,9 +37,8 @@
 // pdl_wait() until the predecessor has completed and its memory is visible. Every kernel
 // launched through pdl_launch() must call pdl_wait() before it touches memory an earlier
 // kernel of the stream writes. pdl_trigger() lets the next kernel launch once every CTA
-// of this grid has triggered (or exited). g_cortex_pdl = 0 turns the attribute off.
-
-extern int g_cortex_pdl;
+// of this grid has triggered (or exited). The PDL knob (cortex_dev.h, tests / A-B only)
+// turns the attribute off.
 
 CORTEX_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 CORTEX_DEVICE void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" :::); }
@@ -51,10 +51,6 @@ CORTEX_DEVICE void tma_prefetch_l2_2d(const void* desc, int c0, int c1) {
                : "memory");
 }
 
-// K blocks of weights a GEMM's weights-only issuer prefetches into L2, beyond its
-// pipeline stages, before the PDL wait (CORTEX_GEMM_L2PF tuning hook; default 0 = off).
-int cortex_gemm_l2pf();
-
 template <typename... KArgs, typename... Args>
 inline cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                               cudaStream_t stream, int cluster_x, Args&&... args) {
@@ -66,7 +62,7 @@ inline cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   cudaLaunchAttribute attr[2];
   int n = 0;
   attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[n].val.programmaticStreamSerializationAllowed = g_cortex_pdl ? 1 : 0;
+  attr[n].val.programmaticStreamSerializationAllowed = g_cortex_knob[CORTEX_KNOB_PDL] ? 1 : 0;
   ++n;
   if (cluster_x > 1) {
     attr[n].id = cudaLaunchAttributeClusterDimension;

@@ -1,5 +1,5 @@
 // Row-wise and element-wise pieces of the decoder step: embedding gather,
-// RMSNorm (optionally gathering rows), RoPE + paged KV append, SwiGLU, and the
+// RMSNorm (optionally gathering rows), RoPE + paged KV append, and the
 // greedy argmax over the vocabulary. All are HBM-bound SIMT kernels with 16-byte
 // vector accesses; arithmetic is fp32, storage bf16.
 #include "common.cuh"
@@ -173,25 +173,6 @@ __global__ void rope_kv_append_kernel(const RopeArgs a) {
   }
 }
 
-// act[t, j] = bf16(silu(g) * u), g = gu[t, j], u = gu[t, F + j]
-__global__ void swiglu_kernel(const __nv_bfloat16* __restrict__ gu, int f, int n_tok,
-                              __nv_bfloat16* __restrict__ act) {
-  const int64_t nvec = static_cast<int64_t>(n_tok) * f / 8;
-  for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < nvec;
-       v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t t = v / (f / 8);
-    const int64_t j = v % (f / 8);
-    const bf16x8 g8 = reinterpret_cast<const bf16x8*>(gu + t * 2 * f)[j];
-    const bf16x8 u8 = reinterpret_cast<const bf16x8*>(gu + t * 2 * f + f)[j];
-    float g[8], u[8], o[8];
-    unpack8(g8, g);
-    unpack8(u8, u);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) o[e] = g[e] / (1.f + __expf(-g[e])) * u[e];
-    reinterpret_cast<bf16x8*>(act + t * f)[j] = pack8(o);
-  }
-}
-
 // Greedy token per row (first index of the maximum). Optionally scatters the token
 // into slot_tok[slot[r]] and hist[slot[r] * hist_stride + hist_pos[r]].
 __global__ void argmax_kernel(const float* __restrict__ logits, int64_t ld, int vocab,
@@ -330,18 +311,6 @@ int32_t cortex_rope_kv_append(const void* qkv, void* q_out, void* cache, int64_t
   a.hkv = hkv;
   if (pdl_launch(rope_kv_append_kernel, n_tok, 256, 0, stream, 1, a) != cudaSuccess)
     return CORTEX_ECUDA;
-  return CORTEX_OK;
-}
-
-int32_t cortex_swiglu(const void* gu, int32_t n_tok, int32_t f, void* act, cudaStream_t stream) {
-  if (!gu || !act || n_tok < 0 || f % 8) return CORTEX_EBADARG;
-  if (n_tok == 0) return CORTEX_OK;
-  const int64_t nvec = static_cast<int64_t>(n_tok) * f / 8;
-  int64_t grid = (nvec + 255) / 256;
-  if (grid > 148 * 16) grid = 148 * 16;
-  swiglu_kernel<<<static_cast<int>(grid), 256, 0, stream>>>(
-      reinterpret_cast<const __nv_bfloat16*>(gu), f, n_tok, reinterpret_cast<__nv_bfloat16*>(act));
-  CORTEX_CHECK_LAUNCH();
   return CORTEX_OK;
 }
 

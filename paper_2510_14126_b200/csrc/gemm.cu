@@ -311,18 +311,11 @@ int32_t cortex_gemm_2sm_launch(const void* tmap_w, const void* tmap_x, int32_t M
                                uint64_t workspace_bytes, int32_t* counters, int32_t n_counters,
                                cudaStream_t stream);
 
-extern "C" int32_t cortex_gemm_splitk_plan(int32_t M, int32_t N, int32_t K, int32_t* tn_out);
 extern "C" int32_t cortex_gemm_splitk_launch(const void* tmap_w, const void* tmap_x, int32_t M,
                                              int32_t N, int32_t K, void* out, int32_t ldo,
                                              int32_t out_f32, const void* residual, int32_t ldr,
                                              float* workspace, uint64_t workspace_bytes,
                                              cudaStream_t stream);
-
-namespace {
-// 0 auto, 1 force the 1-SM (split-K) kernel, 2 force 2-SM when legal, 3 force the
-// cluster split-K 2-SM kernel when it has a plan
-int g_gemm_mode = 0;
-}
 
 extern "C" {
 
@@ -331,19 +324,14 @@ extern "C" {
 // (M > 128, compute bound; needs N % 256 == 0).
 // 3 = cluster split-K 2-SM kernel (gemm_splitk.cu: decode-sized M with few 256-row tiles).
 int32_t cortex_gemm_path(int32_t M, int32_t N, int32_t K) {
+  // knob GEMM_MODE (tests): 0 auto, 1 force 1-SM, 2 force 2-SM when legal, 3 prefer split-K
+  const int mode = g_cortex_knob[CORTEX_KNOB_GEMM_MODE];
   const bool legal2 = (N % 256) == 0;
-  if (g_gemm_mode == 1 || !legal2) return 1;
-  if (g_gemm_mode == 2) return 2;
-  if (cortex_gemm_splitk_plan(M, N, K, nullptr) >= 1) return 3;
-  if (g_gemm_mode == 3) return 2;
+  if (mode == 1 || !legal2) return 1;
+  if (mode == 2) return 2;
+  if (cortex_gemm_splitk_plan(M, N, K, nullptr, nullptr, nullptr) >= 1) return 3;
+  if (mode == 3) return 2;
   return M > 128 ? 2 : 1;
-}
-
-// Test hook: 0 auto, 1 force 1-SM, 2 force 2-SM, 3 prefer the cluster split-K kernel.
-int32_t cortex_gemm_set_mode(int32_t mode) {
-  if (mode < 0 || mode > 3) return CORTEX_EBADARG;
-  g_gemm_mode = mode;
-  return CORTEX_OK;
 }
 
 // Encode a 2-D bf16 TMA descriptor (128 bytes, written to tmap_out) over a

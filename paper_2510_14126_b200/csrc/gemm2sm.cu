@@ -504,29 +504,13 @@ int g_num_sms = 0;
 
 // Tile width (m) and mode the 2-SM GEMM uses for a problem: the lowest modelled
 // time over TN of whole tiles (waves x (TN + 32)). Stream-K is only used when forced
-// (cortex_gemm_set_stream_k / CORTEX_GEMM_SK=1): it balances the MMA work, but the
-// head pair's fix-up epilogue (reading the partials) measured ~5 us per 32-row chunk
-// at the end of the kernel, so e.g. the down projection at M = 700 takes 107 us vs
-// 73 us in whole tiles (benchmarks/gemm_trace.py with a -DCORTEX_GEMM_TRACE build).
-static int g_sk_force = -2;
-
-int32_t cortex_gemm_set_stream_k(int32_t force) {
-  if (force < -1 || force > 1) return CORTEX_EBADARG;
-  g_sk_force = force;
-  return CORTEX_OK;
-}
-
+// (knob GEMM_STREAM_K = 1): it balances the MMA work, but the head pair's fix-up
+// epilogue (reading the partials) measured ~5 us per 32-row chunk at the end of the
+// kernel, so e.g. the down projection at M = 700 takes 107 us vs 73 us in whole tiles
+// (benchmarks/gemm_trace.py with a -DCORTEX_GEMM_TRACE build).
 void cortex_gemm2_plan(int M, int N, int K, int n_sms, int* tn_out, int* sk_out) {
-  if (g_sk_force == -2) {
-    const char* e = getenv("CORTEX_GEMM_SK");
-    g_sk_force = e ? atoi(e) : -1;
-  }
-  const int force = g_sk_force == 1 ? 1 : 0;
-  static int tn_force = -2;  // tuning hook: CORTEX_GEMM_TN pins the token tile width
-  if (tn_force == -2) {
-    const char* e = getenv("CORTEX_GEMM_TN");
-    tn_force = e ? atoi(e) : -1;
-  }
+  const int force = g_cortex_knob[CORTEX_KNOB_GEMM_STREAM_K] == 1 ? 1 : 0;
+  const int tn_force = g_cortex_knob[CORTEX_KNOB_GEMM_TN];  // tuning: pin the token tile
   if (tn_force > 0) {
     *tn_out = tn_force;
     *sk_out = force;
@@ -599,7 +583,7 @@ int32_t cortex_gemm_2sm_launch(const void* tmap_w, const void* tmap_x, int32_t M
   a.total_units = num_tiles * (K / kBK);
   a.workspace = workspace;
   a.flags = counters;
-  a.l2pf = cortex_gemm_l2pf();
+  a.l2pf = g_cortex_knob[CORTEX_KNOB_GEMM_L2PF];
   const auto* tw = reinterpret_cast<const CUtensorMap*>(tmap_w);
   const auto* tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
   switch (tn) {

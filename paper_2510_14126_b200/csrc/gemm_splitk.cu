@@ -371,25 +371,7 @@ int32_t launch_sk(const CUtensorMap* tw, const CUtensorMap* tx, const SkArgs& a,
   return CORTEX_OK;
 }
 
-int g_sk_ks_force = -1;  // test / tuning hooks: force the split count / token tiles
-int g_sk_mt_force = -1;
-int g_sk_nw_force = -1;
-// -2: read CORTEX_SK_ISSUE once (default 2; 1, 2 and 4 issuers measured within noise of
-// each other at M = 64 ... 256 - the decode GEMMs are bound by L2 throughput, weights
-// plus the token rows every weight tile re-reads, not by TMA issue)
-int g_sk_issue = -2;
-
 }  // namespace
-
-int cortex_gemm_l2pf() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CORTEX_GEMM_L2PF");
-    v = e ? atoi(e) : 0;  // measured: 0 best (profiles/r1e_gemm_l2pf_sweep.jsonl)
-    if (v < 0) v = 0;
-  }
-  return v;
-}
 
 extern "C" {
 
@@ -405,8 +387,11 @@ extern "C" {
 //   * the fp32 partials (ks x M x N x 4 bytes) must stay small next to the weights.
 // Measured at M = 16 ... 256 (benchmarks/gemm_sk_sweep.py): 0.7-0.85x the time of the
 // whole-tile 2-SM kernel for o / down / qkv, 0.45-0.6x the 1-SM split-K kernel.
-int32_t cortex_gemm_splitk_plan3(int32_t M, int32_t N, int32_t K, int32_t* tn_out,
-                                 int32_t* mt_out, int32_t* nw_out) {
+int32_t cortex_gemm_splitk_plan(int32_t M, int32_t N, int32_t K, int32_t* tn_out,
+                                int32_t* mt_out, int32_t* nw_out) {
+  const int g_sk_mt_force = g_cortex_knob[CORTEX_KNOB_SK_MT];
+  const int g_sk_ks_force = g_cortex_knob[CORTEX_KNOB_SK_KS];
+  const int g_sk_nw_force = g_cortex_knob[CORTEX_KNOB_SK_NW];
   if (M <= 0 || M > 256 || N % kPairN || K % kBK) return 0;
   const int total_kb = K / kBK;
   const int mt = g_sk_mt_force > 0 ? g_sk_mt_force : 1;
@@ -437,41 +422,12 @@ int32_t cortex_gemm_splitk_plan3(int32_t M, int32_t N, int32_t K, int32_t* tn_ou
   return ks;
 }
 
-int32_t cortex_gemm_splitk_plan2(int32_t M, int32_t N, int32_t K, int32_t* tn_out,
-                                 int32_t* mt_out) {
-  return cortex_gemm_splitk_plan3(M, N, K, tn_out, mt_out, nullptr);
-}
-
-int32_t cortex_gemm_splitk_plan(int32_t M, int32_t N, int32_t K, int32_t* tn_out) {
-  return cortex_gemm_splitk_plan2(M, N, K, tn_out, nullptr);
-}
-
-// Tuning / test hook: pin the split count (2..4) and the number of token tiles (1..4);
-// -1 = automatic.
-int32_t cortex_gemm_splitk_force(int32_t ks) {
-  if (ks < -1 || ks > 4 || ks == 0 || ks == 1) return CORTEX_EBADARG;
-  g_sk_ks_force = ks;
-  return CORTEX_OK;
-}
-
-int32_t cortex_gemm_splitk_force_nw(int32_t nw) {
-  if (nw != -1 && nw != 2) return CORTEX_EBADARG;
-  g_sk_nw_force = nw;
-  return CORTEX_OK;
-}
-
-int32_t cortex_gemm_splitk_force_mt(int32_t mt) {
-  if (mt < -1 || mt > 4 || mt == 0) return CORTEX_EBADARG;
-  g_sk_mt_force = mt;
-  return CORTEX_OK;
-}
-
 int32_t cortex_gemm_splitk_launch(const void* tmap_w, const void* tmap_x, int32_t M, int32_t N,
                                   int32_t K, void* out, int32_t ldo, int32_t out_f32,
                                   const void* residual, int32_t ldr, float* workspace,
                                   uint64_t workspace_bytes, cudaStream_t stream) {
   int tn = 0, mt = 1, nw = 1;
-  const int ks = cortex_gemm_splitk_plan3(M, N, K, &tn, &mt, &nw);
+  const int ks = cortex_gemm_splitk_plan(M, N, K, &tn, &mt, &nw);
   if (ks < 1 || !workspace) return CORTEX_EBADARG;
   const int total_kb = K / kBK;
   const int tiles = N / (kPairN * nw) * mt;
@@ -490,13 +446,11 @@ int32_t cortex_gemm_splitk_launch(const void* tmap_w, const void* tmap_x, int32_
   a.kb_per = (total_kb + ks - 1) / ks;
   a.m_tiles = mt;
   a.ws = workspace;
-  if (g_sk_issue == -2) {
-    const char* e = getenv("CORTEX_SK_ISSUE");
-    g_sk_issue = e ? atoi(e) : 2;
-    if (g_sk_issue != 1 && g_sk_issue != 4) g_sk_issue = 2;
-  }
-  a.n_issue = g_sk_issue;
-  a.l2pf = cortex_gemm_l2pf();
+  // TMA issuers (knob SK_ISSUE, default 2: 1, 2 and 4 issuers measured within noise of
+  // each other at M = 64 ... 256 - the decode GEMMs are bound by L2 throughput, weights
+  // plus the token rows every weight tile re-reads, not by TMA issue)
+  a.n_issue = g_cortex_knob[CORTEX_KNOB_SK_ISSUE];
+  a.l2pf = g_cortex_knob[CORTEX_KNOB_GEMM_L2PF];
   const auto* tw = reinterpret_cast<const CUtensorMap*>(tmap_w);
   const auto* tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
   if (nw == 2) {

@@ -219,17 +219,44 @@ __global__ void popcount_kernel(const uint32_t* bitmap, int nwords, int* out_fre
 
 }  // namespace
 
-int g_cortex_pdl = 1;
+// Tuning / test knobs (cortex_dev.h) with the product defaults.
+int g_cortex_knob[CORTEX_KNOB_COUNT] = {
+    /* PDL */ 1, /* GEMM_MODE */ 0, /* GEMM_STREAM_K */ -1, /* GEMM_TN */ -1,
+    /* GEMM_L2PF */ 0, /* SK_KS */ -1, /* SK_MT */ -1, /* SK_NW */ -1, /* SK_ISSUE */ 2,
+    /* FMHA_2Q */ -1, /* FMHA_PLO */ 1};
+
+namespace {
+bool knob_ok(int knob, int v) {
+  switch (knob) {
+    case CORTEX_KNOB_PDL: return v == 0 || v == 1;
+    case CORTEX_KNOB_GEMM_MODE: return v >= 0 && v <= 3;
+    case CORTEX_KNOB_GEMM_STREAM_K: return v >= -1 && v <= 1;
+    case CORTEX_KNOB_GEMM_TN: return v == -1 || (v >= 64 && v <= 256 && v % 32 == 0);
+    case CORTEX_KNOB_GEMM_L2PF: return v >= 0 && v <= 64;
+    case CORTEX_KNOB_SK_KS: return v == -1 || (v >= 2 && v <= 4);
+    case CORTEX_KNOB_SK_MT: return v == -1 || (v >= 1 && v <= 4);
+    case CORTEX_KNOB_SK_NW: return v == -1 || v == 2;
+    case CORTEX_KNOB_SK_ISSUE: return v == 1 || v == 2 || v == 4;
+    case CORTEX_KNOB_FMHA_2Q: return v >= -1 && v <= 1;
+    case CORTEX_KNOB_FMHA_PLO: return v == 0 || v == 1;
+    default: return false;
+  }
+}
+}  // namespace
 
 extern "C" {
 
-int32_t cortex_abi_version(void) { return 100; }
+int32_t cortex_abi_version(void) { return 101; }
 
-// Programmatic dependent launch of the decoder-step kernels: 1 on (default), 0 off.
-int32_t cortex_set_pdl(int32_t on) {
-  if (on != 0 && on != 1) return CORTEX_EBADARG;
-  g_cortex_pdl = on;
+int32_t cortex_dev_set_knob(int32_t knob, int32_t value) {
+  if (!knob_ok(knob, value)) return CORTEX_EBADARG;
+  g_cortex_knob[knob] = value;
   return CORTEX_OK;
+}
+
+int32_t cortex_dev_get_knob(int32_t knob) {
+  if (knob < 0 || knob >= CORTEX_KNOB_COUNT) return CORTEX_EBADARG;
+  return g_cortex_knob[knob];
 }
 
 int32_t cortex_kv_alloc(uint32_t* bitmap, int32_t nblocks, int32_t id_base,

@@ -107,19 +107,28 @@ def gemm_path(M: int, N: int, K: int) -> int:
     return int(lib().cortex_gemm_path(M, N, K))
 
 
-def gemm_set_mode(mode: int) -> None:
-    _check(lib().cortex_gemm_set_mode(mode), "cortex_gemm_set_mode")
+def gemm_set_mode(mode: int) -> int:
+    """Test hook: 0 auto, 1 force 1-SM, 2 force 2-SM, 3 prefer cluster split-K."""
+    return _lib.set_knob("GEMM_MODE", mode)
 
 
-def fmha_set_2q(on: int) -> None:
+def fmha_set_2q(on: int) -> int:
     """-1: per-launch choice (default), 1: two Q tiles per CTA in the tcgen05 attention,
-    0: one."""
-    _check(lib().cortex_fmha_set_2q(on), "cortex_fmha_set_2q")
+    0: one (the two-tile kernel needs FMHA_PLO = 0)."""
+    return _lib.set_knob("FMHA_2Q", on)
 
 
-def gemm_set_stream_k(force: int) -> None:
+def gemm_set_stream_k(force: int) -> int:
     """-1 automatic, 0 whole tiles, 1 stream-K (2-SM kernel scheduling)."""
-    _check(lib().cortex_gemm_set_stream_k(force), "cortex_gemm_set_stream_k")
+    return _lib.set_knob("GEMM_STREAM_K", force)
+
+
+def splitk_plan(M: int, N: int, K: int) -> tuple[int, int, int, int]:
+    """(splits, token tile, token tiles, weight sub-tiles) of the cluster split-K kernel."""
+    tn, mt, nw = ctypes.c_int32(0), ctypes.c_int32(0), ctypes.c_int32(0)
+    ks = int(lib().cortex_gemm_splitk_plan(M, N, K, ctypes.byref(tn), ctypes.byref(mt),
+                                           ctypes.byref(nw)))
+    return ks, tn.value, mt.value, nw.value
 
 
 def gemm(wmap: TensorMap, xmap: TensorMap, M: int, out: torch.Tensor, ws: GemmWorkspace,
@@ -170,12 +179,6 @@ def rope_kv_append(qkv, q_out, cache, k_row0, v_row0, table, tok_pos, tok_row, t
         ),
         "cortex_rope_kv_append",
     )
-
-
-def swiglu(gu: torch.Tensor, n_tok: int, act: torch.Tensor, stream=None) -> None:
-    f = act.shape[1]
-    _check(lib().cortex_swiglu(gu.data_ptr(), n_tok, f, act.data_ptr(), _stream(stream)),
-           "cortex_swiglu")
 
 
 def argmax(logits: torch.Tensor, n_rows: int, vocab: int, out_tok: torch.Tensor | None = None,
@@ -229,7 +232,7 @@ def paged_decode_attn(kvmap: TensorMap, q, table, seq_row, seq_prefix, seq_kvlen
         g = (_ptr(groups[0]), _ptr(groups[1]), _ptr(groups[2]), _ptr(groups[3])) + tuple(groups[4:])
     f = (None, 0, 0) if flat is None else (_ptr(flat[0]), int(flat[1]), int(flat[2]))
     _check(
-        lib().cortex_paged_decode_attn_flat(
+        lib().cortex_paged_decode_attn(
             kvmap.ptr, q.data_ptr(), table.data_ptr(), table.stride(0), seq_row.data_ptr(),
             seq_prefix.data_ptr(), seq_kvlen.data_ptr(), *f, n_seqs, n_kv_heads, group, k_row0,
             v_row0, scale, o_part.data_ptr(), lse_part.data_ptr(), max_splits, out.data_ptr(),

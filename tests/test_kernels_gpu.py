@@ -151,10 +151,12 @@ def test_gemm_splitk_cluster(cuda, ks, M, N, K):
     r = torch.randn(M, N, generator=g, device=cuda)
     ws = o.GemmWorkspace(cuda)
     o.gemm_set_mode(3)
-    assert L.cortex_gemm_splitk_force(ks) == 0
+    from paper_2510_14126_b200 import _lib
+
+    _lib.set_knob("SK_KS", ks)
     try:
         kb = K // 64
-        got = L.cortex_gemm_splitk_plan(M, N, K, None)
+        got = o.splitk_plan(M, N, K)[0]
         if ks > 0 and got:  # the forced count, or no plan (it would not fit one wave)
             assert got == ks and (got - 1) * -(-kb // got) < kb
         assert got != 1  # (no split only when forced: see test_gemm_splitk_nw2)
@@ -169,7 +171,7 @@ def test_gemm_splitk_cluster(cuda, ks, M, N, K):
         torch.cuda.synchronize()
     finally:
         o.gemm_set_mode(0)
-        L.cortex_gemm_splitk_force(-1)
+        _lib.set_knob("SK_KS", -1)
     assert path == (3 if got >= 1 else 2)
     ref = x[:M].float() @ w.float().T
     assert torch.isfinite(out.float()).all()
@@ -189,18 +191,20 @@ def test_gemm_splitk_nw2(cuda, M, N, K):
     x = torch.randn(max(M, 32), K, generator=g, device=cuda).to(torch.bfloat16)
     w = (torch.randn(N, K, generator=g, device=cuda) * 0.05).to(torch.bfloat16)
     ws = o.GemmWorkspace(cuda)
-    assert L.cortex_gemm_splitk_force_nw(2) == 0
+    from paper_2510_14126_b200 import _lib
+
+    _lib.set_knob("SK_NW", 2)
     try:
-        nw = ctypes.c_int32()
-        assert L.cortex_gemm_splitk_plan3(M, N, K, None, None, ctypes.byref(nw)) == 1
-        assert nw.value == 2 and o.gemm_path(M, N, K) == 3
+        ks, _, _, nw = o.splitk_plan(M, N, K)
+        assert ks == 1
+        assert nw == 2 and o.gemm_path(M, N, K) == 3
         out = torch.full((M, N), float("nan"), device=cuda, dtype=torch.bfloat16)
         o.gemm(o.weight_map(w), o.act_map(x), M, out, ws)
         act = torch.full((M, N // 2), float("nan"), device=cuda, dtype=torch.bfloat16)
         o.gemm(o.weight_map(o.interleave_gate_up(w)), o.act_map(x), M, act, ws, swiglu=True)
         torch.cuda.synchronize()
     finally:
-        L.cortex_gemm_splitk_force_nw(-1)
+        _lib.set_knob("SK_NW", -1)
     ref = x[:M].float() @ w.float().T
     assert rel(out, ref) < 4e-3
     gg, uu = ref[:, :N // 2], ref[:, N // 2:]
@@ -388,7 +392,10 @@ def test_cascade_decode_attention(cuda, group, plens, impl):
     ga = np.asarray(grp, dtype=np.int32).reshape(-1, 4).T
     groups = (dev(ga[0]), dev(ga[1]), dev(ga[2]), dev(ga[3]), len(grp), int(ga[3].max()), pslots)
     k0, v0 = _rows(0, nb, hkv)
+    from paper_2510_14126_b200 import _lib
+
     o.fmha_set_2q(0 if impl == "tc1" else 1)
+    plo = _lib.set_knob("FMHA_PLO", 1 if impl == "tc1" else 0)  # two tiles: bf16 P only
     try:
         o.paged_decode_attn(o.kv_map(cache.view(-1, 128)), q, table, dev(seq_row), dev(seq_pre),
                             dev(seq_kv), B, hkv, group, k0, v0, 1 / math.sqrt(128), o_part,
@@ -396,6 +403,7 @@ def test_cascade_decode_attention(cuda, group, plens, impl):
                             qmap=o.QMap(q, hq, group) if impl != "mma" else None, flat=plan)
     finally:
         o.fmha_set_2q(-1)
+        _lib.set_knob("FMHA_PLO", plo)
     torch.cuda.synchronize()
     for b in range(B):
         k, v = _logical_kv(cache, 0, table[seq_row[b]].cpu(), seq_pre[b], seq_kv[b])
@@ -432,11 +440,15 @@ def test_paged_prefill_attention(cuda, group, impl):
     if impl == "mma":
         o.paged_prefill_attn(kvmap, q, out, *args)
     else:
+        from paper_2510_14126_b200 import _lib
+
         o.fmha_set_2q(0 if impl == "tc1" else 1)
+        plo = _lib.set_knob("FMHA_PLO", 1 if impl == "tc1" else 0)  # two tiles: bf16 P
         try:
             o.fmha_prefill(kvmap, o.QMap(q, hq, group), out, *args)
         finally:
             o.fmha_set_2q(-1)
+            _lib.set_knob("FMHA_PLO", plo)
     torch.cuda.synchronize()
     for b, (prefix, kvlen) in enumerate(specs):
         k, v = _logical_kv(cache, 0, table[b].cpu(), prefix, kvlen)

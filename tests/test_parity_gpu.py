@@ -165,7 +165,7 @@ def _stagesim():
     a `stagesim` package is accepted, then site-packages."""
     root = Path(__file__).resolve().parents[1]
     base = root / "baseline" / "_ref"
-    cands = [p.parent for p in sorted(base.rglob("stagesim/__init__.py"))] if base.exists() else []
+    cands = [p.parent.parent for p in sorted(base.rglob("stagesim/__init__.py"))] if base.exists() else []
     for cand in cands:
         if str(cand) not in sys.path:
             sys.path.insert(0, str(cand))

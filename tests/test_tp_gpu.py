@@ -111,11 +111,13 @@ def _ipc_rank(rank: int, port: int, out_dir: str) -> None:
 
     # both ranks are time-sliced on one GPU: programmatic dependent launch off there
     # ("Several runtimes time-sliced on ONE GPU"); results do not depend on it
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), CORTEX_PDL="0")
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=2)
     from paper_2510_14126_b200 import ops
 
-    ops.lib().cortex_set_pdl(0)  # (also if the library was loaded before the env was set)
+    from paper_2510_14126_b200 import _lib
+
+    _lib.set_knob("PDL", 0)
     dev = torch.device("cuda:0")
     torch.cuda.set_device(dev)
     comm = TpComm(dev, rank, 2, tp_script.MAX_TOKENS, TINY_TP.d_model)
