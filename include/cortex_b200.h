@@ -112,7 +112,11 @@ int32_t cortex_tmap_encode_2d_bf16(void* tmap_out, const void* gptr, uint64_t ro
  * tmap_w over W [N, K] with box (128, 64); tmap_x over X [>= M, K] with box (16, 64).
  * out_f32: 0 = bf16 out, 1 = fp32 out, 2 = fused SwiGLU: W's rows are interleaved in
  * blocks of 64 gate rows then 64 matching up rows, and out[m, f] (bf16, N/2 features) =
- * silu(g) * u with g, u the fp32 accumulators (no residual).
+ * silu(g) * u with g, u the fp32 accumulators (no residual); 3 = greedy-token partials
+ * (the lm_head of a decode step, EngineState.advance_decode's emitted token): out is
+ * float2 [M, ldo = N / 128] of (max, first index of the max as int bits) of each
+ * 128-column chunk of the row, the full logits are never written (no residual);
+ * cortex_argmax_partials reduces them.
  * workspace / counters: the split-K partials and the per-tile arrival counters (kept
  * zeroed) of the decode-sized kernels; 16 Mi floats and 64 Ki counters cover every
  * shape of the Llama-3-8B step (GemmWorkspace in ops.py). */
@@ -120,6 +124,33 @@ int32_t cortex_gemm_bf16(const void* tmap_w, const void* tmap_x, int32_t M, int3
                          void* out, int32_t ldo, int32_t out_f32, const void* residual,
                          int32_t ldr, float* workspace, uint64_t workspace_bytes,
                          int32_t* counters, int32_t n_counters, cortex_stream_t stream);
+
+/* QKV projection with RoPE and the paged KV append fused into the GEMM epilogue (the
+ * per-token KV write of EngineState.admit's prefill and advance_decode's decode steps,
+ * engines.py:142-194): W is [N = (hq + 2 hkv) * 128, K] ([q heads | k heads | v heads]);
+ * for token m the accumulators are rounded to bf16, q / k heads rotated (rotate-half,
+ * position tok_pos[m], tables cos_tab / sin_tab [max_pos, 64] fp32) and rounded again,
+ * q written to q_out [M, hq, 128] and k / v to the token's paged slot (block
+ * table[tok_row[m]][tok_col[m]], offset tok_off[m]) of the layer's K / V plane (128-wide
+ * rows k_row0 / v_row0 of cache). The qkv activation is never written. */
+typedef struct {
+  void* q_out;
+  void* cache;
+  int64_t k_row0, v_row0;
+  const int32_t* table;
+  int32_t table_stride;
+  const int32_t* tok_pos;
+  const int32_t* tok_row;
+  const int32_t* tok_col;
+  const int32_t* tok_off;
+  const float* cos_tab;
+  const float* sin_tab;
+  int32_t hq, hkv;
+} cortex_rope_epilogue_t;
+int32_t cortex_gemm_qkv_rope(const void* tmap_w, const void* tmap_x, int32_t M, int32_t N,
+                             int32_t K, const cortex_rope_epilogue_t* epi, float* workspace,
+                             uint64_t workspace_bytes, int32_t* counters, int32_t n_counters,
+                             cortex_stream_t stream);
 
 /* out[t] (fp32, the residual stream) = emb[tokens[index ? index[t] : t]] (bf16 table). */
 int32_t cortex_embed(const void* emb, const int32_t* tokens, const int32_t* index, int32_t n_tok,
@@ -137,6 +168,13 @@ int32_t cortex_rope_kv_append(const void* qkv, void* q_out, void* cache, int64_t
                               const int32_t* tok_col, const int32_t* tok_off,
                               const float* cos_tab, const float* sin_tab, int32_t n_tok,
                               int32_t hq, int32_t hkv, cortex_stream_t stream);
+
+/* Greedy token per row from cortex_gemm_bf16's out mode 3 partials (float2 [n_rows,
+ * n_chunks]); the same token as cortex_argmax over the full logits. */
+int32_t cortex_argmax_partials(const void* partials, int32_t n_chunks, int32_t n_rows,
+                               int32_t* out_tok, const int32_t* slot, int32_t* slot_tok,
+                               int32_t* hist, int32_t hist_stride, const int32_t* hist_pos,
+                               cortex_stream_t stream);
 
 /* Greedy token per row; optional scatter into per-slot state. */
 int32_t cortex_argmax(const float* logits, int64_t ld, int32_t n_rows, int32_t vocab,

@@ -31,10 +31,12 @@ SIGNATURES: dict[str, list] = {
     "cortex_table_copy_h": [P, I32, P, P, P, P, I32, P],
     "cortex_tmap_encode_2d_bf16": [P, P, U64, U64, U64, ctypes.c_uint32, ctypes.c_uint32],
     "cortex_gemm_bf16": [P, P, I32, I32, I32, P, I32, I32, P, I32, P, U64, P, I32, P],
+    "cortex_gemm_qkv_rope": [P, P, I32, I32, I32, P, P, U64, P, I32, P],
     "cortex_embed": [P, P, P, I32, I32, P, P],
     "cortex_rmsnorm": [P, P, I32, P, I32, F32, P, P],
     "cortex_rope_kv_append": [P, P, P, I64, I64, P, I32, P, P, P, P, P, P, I32, I32, I32, P],
     "cortex_argmax": [P, I64, I32, I32, P, P, P, P, I32, P, P],
+    "cortex_argmax_partials": [P, I32, I32, P, P, P, P, I32, P, P],
     "cortex_f32_gemm": [P, I32, P, I32, I32, I32, P, I32, P, I32, I32, P],
     "cortex_f32_embed": [P, P, P, I32, I32, P, P],
     "cortex_f32_rmsnorm": [P, P, I32, P, I32, F32, P, P],
@@ -75,6 +77,14 @@ DEV_SIGNATURES: dict[str, list] = {
 KNOBS = {name: i for i, name in enumerate(
     ["PDL", "GEMM_MODE", "GEMM_STREAM_K", "GEMM_TN", "GEMM_L2PF", "SK_KS", "SK_MT", "SK_NW",
      "SK_ISSUE", "FMHA_2Q", "FMHA_PLO"])}
+
+class RopeEpilogue(ctypes.Structure):
+    """cortex_rope_epilogue_t (include/cortex_b200.h)."""
+
+    _fields_ = [("q_out", P), ("cache", P), ("k_row0", I64), ("v_row0", I64), ("table", P),
+                ("table_stride", I32), ("tok_pos", P), ("tok_row", P), ("tok_col", P),
+                ("tok_off", P), ("cos_tab", P), ("sin_tab", P), ("hq", I32), ("hkv", I32)]
+
 
 STATUS_NAMES = {0: "ok", -1: "bad argument", -2: "CUDA error", -3: "out of KV blocks",
                 -4: "unsupported",

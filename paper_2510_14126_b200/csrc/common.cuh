@@ -79,6 +79,43 @@ inline cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 // --------------------------------------------------------------------------
 // generic
 
+// ---- greedy-token partials (the lm_head GEMM's argmax epilogue, out mode 3) ----
+// (max, first index of the max) of four consecutive columns col .. col + 3; NaN never
+// wins a comparison, so a chunk without a finite value keeps index INT_MAX.
+CORTEX_DEVICE void best_of4(const float4 v, int col, float& best, int& bi) {
+  best = -INFINITY;
+  bi = 0x7fffffff;
+  if (v.x > best) { best = v.x; bi = col; }
+  if (v.y > best) { best = v.y; bi = col + 1; }
+  if (v.z > best) { best = v.z; bi = col + 2; }
+  if (v.w > best) { best = v.w; bi = col + 3; }
+}
+
+// Warp-wide (max, first index) reduction; every lane ends with the result.
+CORTEX_DEVICE void warp_argmax(float& best, int& bi) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+}
+
+// One warp covers a 128-column output row (lane -> columns col .. col + 3): write its
+// (max, first index) as the row's partial for column chunk col0 / 128.
+CORTEX_DEVICE void store_argmax_partial(float2* part, int ld, int row, int col0, const float4 v,
+                                        int col) {
+  float best;
+  int bi;
+  best_of4(v, col, best, bi);
+  warp_argmax(best, bi);
+  if ((threadIdx.x & 31) == 0)
+    part[static_cast<size_t>(row) * ld + col0 / 128] = make_float2(best, __int_as_float(bi));
+}
+
 CORTEX_DEVICE uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -293,6 +330,69 @@ CORTEX_DEVICE uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
+
+// ---- RoPE + paged KV append in the QKV GEMM's epilogue (out mode 4) ----
+// The QKV projection's 128-column chunks are whole heads ([q heads | k heads | v heads]
+// x 128). For one token row m and head h, lane l holds the fp32 accumulators of dims
+// 4l .. 4l + 3; the epilogue rounds them to bf16 (the unfused path's qkv activation),
+// rotates q / k heads (rotate-half: dim i pairs with i + 64, i.e. lane l with l ^ 16),
+// rounds again and stores q into q_out [T, hq, 128] and k / v straight into the token's
+// paged slot (table[tok_row][tok_col], offset tok_off) of the layer's K / V plane.
+struct RopeEpi {
+  __nv_bfloat16* q_out;
+  __nv_bfloat16* cache;
+  int64_t k_row0, v_row0;
+  const int* table;
+  int table_stride;
+  const int* tok_pos;
+  const int* tok_row;
+  const int* tok_col;
+  const int* tok_off;
+  const float* cos_tab;
+  const float* sin_tab;
+  int hq, hkv;
+};
+
+CORTEX_DEVICE float round_bf16(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+
+CORTEX_DEVICE void rope_epilogue_row(const RopeEpi& e, int m, int h, float4 v) {
+  const int lane = threadIdx.x & 31;
+  float x[4] = {round_bf16(v.x), round_bf16(v.y), round_bf16(v.z), round_bf16(v.w)};
+  float y[4];
+  if (h < e.hq + e.hkv) {  // (warp-uniform)
+    const int pos = __ldg(e.tok_pos + m);
+    const int i0 = 4 * (lane & 15);
+    const float4 c = __ldg(reinterpret_cast<const float4*>(e.cos_tab + pos * 64 + i0));
+    const float4 s = __ldg(reinterpret_cast<const float4*>(e.sin_tab + pos * 64 + i0));
+    const float cc[4] = {c.x, c.y, c.z, c.w}, ss[4] = {s.x, s.y, s.z, s.w};
+    const bool upper = lane >= 16;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float p = __shfl_xor_sync(0xffffffffu, x[j], 16);
+      y[j] = upper ? x[j] * cc[j] + p * ss[j] : x[j] * cc[j] - p * ss[j];
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) y[j] = x[j];
+  }
+  __nv_bfloat16* dst;
+  if (h < e.hq) {
+    dst = e.q_out + (static_cast<int64_t>(m) * e.hq + h) * 128;
+  } else {
+    const int block = __ldg(e.table + static_cast<int64_t>(__ldg(e.tok_row + m)) * e.table_stride +
+                            __ldg(e.tok_col + m));
+    const int off = __ldg(e.tok_off + m);
+    const bool is_k = h < e.hq + e.hkv;
+    const int kh = is_k ? h - e.hq : h - e.hq - e.hkv;
+    dst = e.cache + ((is_k ? e.k_row0 : e.v_row0) + (static_cast<int64_t>(block) * e.hkv + kh) * 16 +
+                     off) * 128;
+  }
+  uint2 packed;
+  packed.x = pack_bf16(y[0], y[1]);
+  packed.y = pack_bf16(y[2], y[3]);
+  *reinterpret_cast<uint2*>(dst + 4 * lane) = packed;
+}
+
 
 // (a, b) -> bf16x2 hi = round(a, b) and lo = round((a, b) - hi)
 CORTEX_DEVICE void split_bf16(float a, float b, uint32_t& hi, uint32_t& lo) {

@@ -253,6 +253,51 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int64_t ld, int 
   }
 }
 
+// Greedy token per row from the lm_head GEMM's per-128-column partials (out mode 3):
+// (max, first index) over the row's n_chunks partials, chunk order = column order, so
+// the result is the first index of the row maximum, exactly argmax_kernel's.
+__global__ void argmax_partials_kernel(const float2* __restrict__ part, int n_chunks,
+                                       int* __restrict__ out_tok, const int* __restrict__ slot,
+                                       int* __restrict__ slot_tok, int* __restrict__ hist,
+                                       int hist_stride, const int* __restrict__ hist_pos) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  const int r = blockIdx.x;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int c = threadIdx.x; c < n_chunks; c += blockDim.x) {
+    const float2 p = part[static_cast<size_t>(r) * n_chunks + c];
+    const int i = __float_as_int(p.y);
+    if (p.x > best || (p.x == best && i < bi)) {
+      best = p.x;
+      bi = i;
+    }
+  }
+  warp_argmax(best, bi);
+  if (lane_id() == 0) {
+    sv[warp_id()] = best;
+    si[warp_id()] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x / 32); ++w) {
+      if (sv[w] > best || (sv[w] == best && si[w] < bi)) {
+        best = sv[w];
+        bi = si[w];
+      }
+    }
+    if (bi == 0x7fffffff) bi = 0;  // no finite logit in the row (argmax_kernel's rule)
+    if (out_tok) out_tok[r] = bi;
+    if (slot) {
+      const int s = slot[r];
+      if (slot_tok) slot_tok[s] = bi;
+      if (hist) hist[static_cast<int64_t>(s) * hist_stride + hist_pos[r]] = bi;
+    }
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -310,6 +355,20 @@ int32_t cortex_rope_kv_append(const void* qkv, void* q_out, void* cache, int64_t
   a.hq = hq;
   a.hkv = hkv;
   if (pdl_launch(rope_kv_append_kernel, n_tok, 256, 0, stream, 1, a) != cudaSuccess)
+    return CORTEX_ECUDA;
+  return CORTEX_OK;
+}
+
+int32_t cortex_argmax_partials(const void* partials, int32_t n_chunks, int32_t n_rows,
+                               int32_t* out_tok, const int32_t* slot, int32_t* slot_tok,
+                               int32_t* hist, int32_t hist_stride, const int32_t* hist_pos,
+                               cudaStream_t stream) {
+  if (!partials || n_rows < 0 || n_chunks <= 0) return CORTEX_EBADARG;
+  if (hist && (!slot || !hist_pos)) return CORTEX_EBADARG;
+  if (n_rows == 0) return CORTEX_OK;
+  if (pdl_launch(argmax_partials_kernel, n_rows, 256, 0, stream, 1,
+                 reinterpret_cast<const float2*>(partials), n_chunks, out_tok, slot, slot_tok,
+                 hist, hist_stride, hist_pos) != cudaSuccess)
     return CORTEX_ECUDA;
   return CORTEX_OK;
 }

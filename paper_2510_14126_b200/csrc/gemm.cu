@@ -37,6 +37,7 @@ struct GemmArgs {
   float* workspace;
   int* counters;
   int evict_first_w;
+  RopeEpi rope;  // out mode 4 (QKV: RoPE + paged KV append in the epilogue)
 };
 
 template <int TN, int STAGES>
@@ -54,6 +55,18 @@ struct GemmSmem {
 // four rows' loads are issued before any store (out may alias residual).
 CORTEX_DEVICE void epilogue_rows(const GemmArgs& a, const float* stile, int m0, int rows, int r0,
                                  int lane, int col) {
+  if (a.out_f32 == 4) {  // QKV: the tile's 128 columns are one head
+    for (int r = r0; r < rows; r += 4)
+      rope_epilogue_row(a.rope, m0 + r, (col - 4 * lane) / kBlockN,
+                        reinterpret_cast<const float4*>(stile + r * kBlockN)[lane]);
+    return;
+  }
+  if (a.out_f32 == 3) {  // greedy-token partials: (max, index) of this tile's 128 columns
+    for (int r = r0; r < rows; r += 4)
+      store_argmax_partial(reinterpret_cast<float2*>(a.out), a.ldo, m0 + r, col - 4 * lane,
+                           reinterpret_cast<const float4*>(stile + r * kBlockN)[lane], col);
+    return;
+  }
   if (a.out_f32 == 2) {  // fused SwiGLU: tile rows = 64 gate + 64 up features
     const int f = (col - 4 * lane) / 2 + 2 * lane;
     for (int r = r0; r < rows; r += 4) {
@@ -309,13 +322,13 @@ int32_t cortex_gemm_2sm_launch(const void* tmap_w, const void* tmap_x, int32_t M
                                int32_t K, void* out, int32_t ldo, int32_t out_f32,
                                const void* residual, int32_t ldr, float* workspace,
                                uint64_t workspace_bytes, int32_t* counters, int32_t n_counters,
-                               cudaStream_t stream);
+                               const RopeEpi* rope, cudaStream_t stream);
 
 extern "C" int32_t cortex_gemm_splitk_launch(const void* tmap_w, const void* tmap_x, int32_t M,
                                              int32_t N, int32_t K, void* out, int32_t ldo,
                                              int32_t out_f32, const void* residual, int32_t ldr,
                                              float* workspace, uint64_t workspace_bytes,
-                                             cudaStream_t stream);
+                                             const RopeEpi* rope, cudaStream_t stream);
 
 extern "C" {
 
@@ -399,19 +412,23 @@ int32_t cortex_gemm_splits(int32_t M, int32_t N, int32_t K) {
 // (elements); out_f32 selects fp32 instead of bf16 output. workspace/counters are only used
 // when cortex_gemm_splits(M, N, K) > 1 (workspace >= splits*M*N floats, counters zeroed,
 // >= n_tiles*m_tiles ints; the kernel leaves them zeroed).
-int32_t cortex_gemm_bf16(const void* tmap_w, const void* tmap_x, int32_t M, int32_t N, int32_t K,
-                         void* out, int32_t ldo, int32_t out_f32, const void* residual,
-                         int32_t ldr, float* workspace, uint64_t workspace_bytes,
-                         int32_t* counters, int32_t n_counters, cudaStream_t stream) {
-  if (!tmap_w || !tmap_x || !out || M <= 0 || N <= 0 || K <= 0 || N % kBlockN || K % kBlockK)
+static int32_t gemm_dispatch(const void* tmap_w, const void* tmap_x, int32_t M, int32_t N,
+                             int32_t K, void* out, int32_t ldo, int32_t out_f32,
+                             const void* residual, int32_t ldr, float* workspace,
+                             uint64_t workspace_bytes, int32_t* counters, int32_t n_counters,
+                             const RopeEpi* rope, cudaStream_t stream) {
+  if (!tmap_w || !tmap_x || (!out && out_f32 != 4) || M <= 0 || N <= 0 || K <= 0 ||
+      N % kBlockN || K % kBlockK || out_f32 < 0 || out_f32 > 4 || (out_f32 >= 2 && residual) ||
+      (out_f32 == 4 && !rope))
     return CORTEX_EBADARG;
-  const int path = cortex_gemm_path(M, N, K);
+  int path = cortex_gemm_path(M, N, K);
+  if (out_f32 == 3 && path == 3) path = M > 128 ? 2 : 1;  // (lm_head never plans split-K)
   if (path == 3)
     return cortex_gemm_splitk_launch(tmap_w, tmap_x, M, N, K, out, ldo, out_f32, residual, ldr,
-                                     workspace, workspace_bytes, stream);
+                                     workspace, workspace_bytes, rope, stream);
   if (path == 2)
     return cortex_gemm_2sm_launch(tmap_w, tmap_x, M, N, K, out, ldo, out_f32, residual, ldr,
-                                  workspace, workspace_bytes, counters, n_counters, stream);
+                                  workspace, workspace_bytes, counters, n_counters, rope, stream);
   GemmArgs a{};
   a.M = M;
   a.N = N;
@@ -427,6 +444,7 @@ int32_t cortex_gemm_bf16(const void* tmap_w, const void* tmap_x, int32_t M, int3
   a.splits = splits;
   a.workspace = workspace;
   a.counters = counters;
+  if (rope) a.rope = *rope;
   const int n_tiles = N / kBlockN;
   if (splits > 1) {
     if (!workspace || !counters ||
@@ -450,6 +468,43 @@ int32_t cortex_gemm_bf16(const void* tmap_w, const void* tmap_x, int32_t M, int3
     case 128: return launch_gemm<128, 5>(tw, tx, a, grid, stream);
     default: return launch_gemm<256, 4>(tw, tx, a, grid, stream);
   }
+}
+
+int32_t cortex_gemm_bf16(const void* tmap_w, const void* tmap_x, int32_t M, int32_t N, int32_t K,
+                         void* out, int32_t ldo, int32_t out_f32, const void* residual,
+                         int32_t ldr, float* workspace, uint64_t workspace_bytes,
+                         int32_t* counters, int32_t n_counters, cudaStream_t stream) {
+  if (out_f32 == 4) return CORTEX_EBADARG;  // (cortex_gemm_qkv_rope)
+  return gemm_dispatch(tmap_w, tmap_x, M, N, K, out, ldo, out_f32, residual, ldr, workspace,
+                       workspace_bytes, counters, n_counters, nullptr, stream);
+}
+
+// QKV projection with RoPE + paged KV append in the epilogue (see the header).
+int32_t cortex_gemm_qkv_rope(const void* tmap_w, const void* tmap_x, int32_t M, int32_t N,
+                             int32_t K, const cortex_rope_epilogue_t* epi, float* workspace,
+                             uint64_t workspace_bytes, int32_t* counters, int32_t n_counters,
+                             cudaStream_t stream) {
+  if (!epi || !epi->q_out || !epi->cache || !epi->table || !epi->tok_pos || !epi->tok_row ||
+      !epi->tok_col || !epi->tok_off || !epi->cos_tab || !epi->sin_tab || epi->hq < 1 ||
+      epi->hkv < 1 || N != (epi->hq + 2 * epi->hkv) * 128)
+    return CORTEX_EBADARG;
+  RopeEpi r{};
+  r.q_out = reinterpret_cast<__nv_bfloat16*>(epi->q_out);
+  r.cache = reinterpret_cast<__nv_bfloat16*>(epi->cache);
+  r.k_row0 = epi->k_row0;
+  r.v_row0 = epi->v_row0;
+  r.table = epi->table;
+  r.table_stride = epi->table_stride;
+  r.tok_pos = epi->tok_pos;
+  r.tok_row = epi->tok_row;
+  r.tok_col = epi->tok_col;
+  r.tok_off = epi->tok_off;
+  r.cos_tab = epi->cos_tab;
+  r.sin_tab = epi->sin_tab;
+  r.hq = epi->hq;
+  r.hkv = epi->hkv;
+  return gemm_dispatch(tmap_w, tmap_x, M, N, K, nullptr, 0, 4, nullptr, 0, workspace,
+                       workspace_bytes, counters, n_counters, &r, stream);
 }
 
 }  // extern "C"

@@ -51,6 +51,7 @@ struct Gemm2Args {
   float* workspace;  // stream-K: [npairs * 2][TN][128] fp32 partials
   int* flags;        // stream-K: [npairs * 2] partial-ready flags, left zeroed
   int l2pf;          // weight K blocks prefetched into L2 beyond the stages (first segment)
+  RopeEpi rope;      // out mode 4 (QKV: RoPE + paged KV append in the epilogue)
 };
 
 struct Seg {
@@ -131,6 +132,27 @@ CORTEX_DEVICE void epi_bar_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memor
 // (out may alias the residual).
 CORTEX_DEVICE void store_chunk(const Gemm2Args& args, const float* staging, int mrow0, int crow,
                                int ew, int lane, int col) {
+  if (args.out_f32 == 4) {  // QKV: this CTA's 128 columns are one head
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int r = ew + 4 * q;
+      if (r < crow)  // (warp-uniform)
+        rope_epilogue_row(args.rope, mrow0 + r, (col - 4 * lane) / 128,
+                          reinterpret_cast<const float4*>(staging + r * 128)[lane]);
+    }
+    return;
+  }
+  if (args.out_f32 == 3) {  // greedy-token partials: (max, index) of this CTA's 128 columns
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int r = ew + 4 * q;
+      if (r < crow)  // (warp-uniform)
+        store_argmax_partial(reinterpret_cast<float2*>(args.out), args.ldo, mrow0 + r,
+                             col - 4 * lane, reinterpret_cast<const float4*>(staging + r * 128)[lane],
+                             col);
+    }
+    return;
+  }
   if (args.out_f32 == 2) {  // fused SwiGLU: each CTA's 128 rows = 64 gate + 64 up features
     const int f = (col - 4 * lane) / 2 + 2 * lane;
 #pragma unroll
@@ -408,7 +430,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
               __stcg(reinterpret_cast<float4*>(ws + static_cast<size_t>(c0 + r) * 128 + 4 * lane),
                      reinterpret_cast<const float4*>(staging + r * 128)[lane]);
           }
-        } else if (args.out_f32 == 2) {  // SwiGLU reads other lanes' columns of the row
+        } else if (args.out_f32 >= 2) {  // SwiGLU / argmax read other lanes' columns
           if (head) {
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
@@ -552,8 +574,8 @@ int32_t cortex_gemm_2sm_launch(const void* tmap_w, const void* tmap_x, int32_t M
                                int32_t K, void* out, int32_t ldo, int32_t out_f32,
                                const void* residual, int32_t ldr, float* workspace,
                                uint64_t workspace_bytes, int32_t* counters, int32_t n_counters,
-                               cudaStream_t stream) {
-  if (N % kPairN || K % kBK || M <= 0) return CORTEX_EBADARG;
+                               const RopeEpi* rope, cudaStream_t stream) {
+  if (N % kPairN || K % kBK || M <= 0 || (out_f32 == 4 && !rope)) return CORTEX_EBADARG;
   if (g_num_sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -584,6 +606,7 @@ int32_t cortex_gemm_2sm_launch(const void* tmap_w, const void* tmap_x, int32_t M
   a.workspace = workspace;
   a.flags = counters;
   a.l2pf = g_cortex_knob[CORTEX_KNOB_GEMM_L2PF];
+  if (rope) a.rope = *rope;
   const auto* tw = reinterpret_cast<const CUtensorMap*>(tmap_w);
   const auto* tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
   switch (tn) {

@@ -44,6 +44,7 @@ struct SkArgs {
   float* ws;    // [tiles][ks][2][TN][128] fp32 partials
   int n_issue;  // TMA issuing threads: 1, 2 (weights | tokens) or 4 (two of each)
   int l2pf;     // weight K blocks prefetched into L2 beyond the stages, before the PDL wait
+  RopeEpi rope;  // out mode 4 (QKV: RoPE + paged KV append in the epilogue)
 };
 
 // NW weight sub-tiles of 256 rows per pair (one MMA each, sharing the staged token rows):
@@ -106,6 +107,10 @@ CORTEX_DEVICE void reduce_rows(const SkArgs& args, const float* base, size_t spl
         sum.y += p[q][i].y;
         sum.z += p[q][i].z;
         sum.w += p[q][i].w;
+      }
+      if (args.out_f32 == 4) {  // QKV: the 128 columns are one head
+        rope_epilogue_row(args.rope, m0 + r, n0 / 128, sum);
+        continue;
       }
       if (swiglu) {  // lanes 0-15 hold gate features, 16-31 the matching ups
         const float ux = __shfl_down_sync(0xffffffffu, sum.x, 16);
@@ -425,10 +430,11 @@ int32_t cortex_gemm_splitk_plan(int32_t M, int32_t N, int32_t K, int32_t* tn_out
 int32_t cortex_gemm_splitk_launch(const void* tmap_w, const void* tmap_x, int32_t M, int32_t N,
                                   int32_t K, void* out, int32_t ldo, int32_t out_f32,
                                   const void* residual, int32_t ldr, float* workspace,
-                                  uint64_t workspace_bytes, cudaStream_t stream) {
+                                  uint64_t workspace_bytes, const RopeEpi* rope,
+                                  cudaStream_t stream) {
   int tn = 0, mt = 1, nw = 1;
   const int ks = cortex_gemm_splitk_plan(M, N, K, &tn, &mt, &nw);
-  if (ks < 1 || !workspace) return CORTEX_EBADARG;
+  if (ks < 1 || !workspace || (out_f32 == 4 && !rope)) return CORTEX_EBADARG;
   const int total_kb = K / kBK;
   const int tiles = N / (kPairN * nw) * mt;
   if (workspace_bytes < static_cast<uint64_t>(tiles) * ks * 2 * nw * tn * 128 * sizeof(float))
@@ -451,6 +457,7 @@ int32_t cortex_gemm_splitk_launch(const void* tmap_w, const void* tmap_x, int32_
   // plus the token rows every weight tile re-reads, not by TMA issue)
   a.n_issue = g_cortex_knob[CORTEX_KNOB_SK_ISSUE];
   a.l2pf = g_cortex_knob[CORTEX_KNOB_GEMM_L2PF];
+  if (rope) a.rope = *rope;
   const auto* tw = reinterpret_cast<const CUtensorMap*>(tmap_w);
   const auto* tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
   if (nw == 2) {

@@ -231,6 +231,11 @@ class GpuWorker:
         self.act = torch.zeros(T, cfg.ffn, dtype=BF16, device=dev)
         self.xn_out = torch.zeros(max_out, d, dtype=BF16, device=dev)
         self.logits = torch.zeros(max_out, cfg.vocab, dtype=torch.float32, device=dev)
+        # greedy tokens straight from the lm_head GEMM's epilogue: (max, index) per
+        # 128-vocab chunk, reduced per row; the full fp32 logits are written only when
+        # `full_logits` is set (parity checks) or an on_forward hook may read them
+        self.lm_part = torch.zeros(max_out, cfg.vocab // 128, dtype=torch.int64, device=dev)
+        self.full_logits = False
         self.out_tok = torch.zeros(max_out, dtype=torch.int32, device=dev)
         self.xn_map = ops.act_map(self.xn)
         self.attn_map = ops.act_map(self.attn)
@@ -593,9 +598,9 @@ class GpuWorker:
             pf_bytes = float(pf_kvlen.sum()) * tok_kv_bytes + 2 * 2 * (T - n_dec) * hq * HEAD_DIM
             pf_flops = 4.0 * hq * HEAD_DIM * pf_keys
 
-        def gemm(name, xmap, M, out, residual=None, swiglu=False):
+        def gemm(name, xmap, M, out, residual=None, swiglu=False, argmax=False):
             e0 = prof.open("gemm") if prof is not None else None
-            ops.gemm(wm[name], xmap, M, out, ws, residual=residual, swiglu=swiglu)
+            ops.gemm(wm[name], xmap, M, out, ws, residual=residual, swiglu=swiglu, argmax=argmax)
             if e0 is not None:
                 N, K = wm[name].rows, wm[name].cols
                 ob = out.element_size() * (2 if residual is not None else 1)
@@ -610,10 +615,16 @@ class GpuWorker:
             if tp is None or li == 0:  # TP: fused into the previous layer's down exchange
                 ops.rmsnorm(x, w[p + "attn_norm"], T, xn, cfg.eps)
                 nl += 1
-            gemm(p + "wqkv", self.xn_map, T, self.qkv)
-            ops.rope_kv_append(self.qkv, self.q, self.cache, k0, v0, self.table, d_pos, d_arow,
-                               d_acol, d_aoff, self.cos, self.sin, T, hq, hkv)
-            nl += 2
+            # QKV GEMM with RoPE + the paged KV append in its epilogue (the qkv activation
+            # is never written)
+            e0 = prof.open("gemm") if prof is not None else None
+            ops.gemm_qkv_rope(wm[p + "wqkv"], self.xn_map, T, ws, self.q, self.cache, k0, v0,
+                              self.table, d_pos, d_arow, d_acol, d_aoff, self.cos, self.sin, hq,
+                              hkv)
+            if e0 is not None:
+                N, K = wm[p + "wqkv"].rows, wm[p + "wqkv"].cols
+                prof.close("gemm", e0, 2.0 * N * K + 2.0 * T * K + 2.0 * T * N, 2.0 * T * N * K)
+            nl += 1
             def prefill_attn(stream=None):
                 if self.tc_attention:
                     ops.fmha_prefill(self.kvmap, self.qmap, self.attn, self.table, d_prow, d_ppre,
@@ -693,9 +704,14 @@ class GpuWorker:
                 nl += 3
         if n_out:
             ops.rmsnorm(x, w["final_norm"], n_out, self.xn_out, cfg.eps, rows=d_orow)
-            gemm("lm_head", self.xn_out_map, n_out, self.logits)
-            ops.argmax(self.logits, n_out, cfg.vocab, out_tok=self.out_tok, slot=d_oslot,
-                       slot_tok=self.slot_tok, hist=self.hist, hist_pos=d_ohist)
+            if self.full_logits or self.on_forward is not None or cfg.vocab % 128:
+                gemm("lm_head", self.xn_out_map, n_out, self.logits)
+                ops.argmax(self.logits, n_out, cfg.vocab, out_tok=self.out_tok, slot=d_oslot,
+                           slot_tok=self.slot_tok, hist=self.hist, hist_pos=d_ohist)
+            else:  # argmax fused into the lm_head epilogue: no logits round trip
+                gemm("lm_head", self.xn_out_map, n_out, self.lm_part, argmax=True)
+                ops.argmax_partials(self.lm_part, n_out, out_tok=self.out_tok, slot=d_oslot,
+                                    slot_tok=self.slot_tok, hist=self.hist, hist_pos=d_ohist)
             nl += 3
         self.launches += nl
         self.steps += 1

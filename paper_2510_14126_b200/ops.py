@@ -132,13 +132,20 @@ def splitk_plan(M: int, N: int, K: int) -> tuple[int, int, int, int]:
 
 
 def gemm(wmap: TensorMap, xmap: TensorMap, M: int, out: torch.Tensor, ws: GemmWorkspace,
-         residual: torch.Tensor | None = None, swiglu: bool = False, stream=None) -> torch.Tensor:
+         residual: torch.Tensor | None = None, swiglu: bool = False, argmax: bool = False,
+         stream=None) -> torch.Tensor:
     """out[:M] = X[:M] @ W^T (+ residual). out is bf16 or fp32 [>=M, N] row-major.
-    swiglu: W rows interleaved (64 gate, 64 up, ...) and out = silu(g) * u, bf16 [>=M, N/2]."""
+    swiglu: W rows interleaved (64 gate, 64 up, ...) and out = silu(g) * u, bf16 [>=M, N/2].
+    argmax: out is the greedy-token partials, int64 [>=M, N/128] (float2 (max, index) per
+    128-column chunk, reduced by argmax_partials); no logits are written."""
     N, K = wmap.rows, wmap.cols
     if xmap.cols != K or M > xmap.rows:
         raise ValueError("gemm shape mismatch")
-    if swiglu:
+    if argmax:
+        if out.dtype != torch.int64 or out.shape[1] != N // 128 or residual is not None:
+            raise ValueError("argmax gemm writes int64 [M, N/128] partials without residual")
+        out_f32 = 3
+    elif swiglu:
         if out.dtype != torch.bfloat16 or out.shape[1] != N // 2 or residual is not None:
             raise ValueError("swiglu gemm writes bf16 [M, N/2] without residual")
         out_f32 = 2
@@ -154,6 +161,23 @@ def gemm(wmap: TensorMap, xmap: TensorMap, M: int, out: torch.Tensor, ws: GemmWo
         "cortex_gemm_bf16",
     )
     return out
+
+
+def gemm_qkv_rope(wmap: TensorMap, xmap: TensorMap, M: int, ws: GemmWorkspace, q_out, cache,
+                  k_row0, v_row0, table, tok_pos, tok_row, tok_col, tok_off, cos_tab, sin_tab,
+                  hq: int, hkv: int, stream=None) -> None:
+    """QKV projection with RoPE + paged KV append in the epilogue (rope_kv_append fused)."""
+    N, K = wmap.rows, wmap.cols
+    if xmap.cols != K or M > xmap.rows or N != (hq + 2 * hkv) * 128:
+        raise ValueError("qkv gemm shape mismatch")
+    e = _lib.RopeEpilogue(q_out.data_ptr(), cache.data_ptr(), k_row0, v_row0, table.data_ptr(),
+                          table.stride(0), tok_pos.data_ptr(), tok_row.data_ptr(),
+                          tok_col.data_ptr(), tok_off.data_ptr(), cos_tab.data_ptr(),
+                          sin_tab.data_ptr(), hq, hkv)
+    _check(lib().cortex_gemm_qkv_rope(wmap.ptr, xmap.ptr, M, N, K, ctypes.byref(e),
+                                      ws.ws.data_ptr(), ws.ws.numel() * 4,
+                                      ws.counters.data_ptr(), ws.counters.numel(),
+                                      _stream(stream)), "cortex_gemm_qkv_rope")
 
 
 def embed(emb: torch.Tensor, tokens: torch.Tensor, n_tok: int, out: torch.Tensor,
@@ -192,6 +216,18 @@ def argmax(logits: torch.Tensor, n_rows: int, vocab: int, out_tok: torch.Tensor 
             _stream(stream),
         ),
         "cortex_argmax",
+    )
+
+
+def argmax_partials(part: torch.Tensor, n_rows: int, out_tok=None, slot=None, slot_tok=None,
+                    hist=None, hist_pos=None, stream=None) -> None:
+    """Greedy token per row from gemm(..., argmax=True) partials (same rule as argmax)."""
+    _check(
+        lib().cortex_argmax_partials(
+            part.data_ptr(), part.shape[1], n_rows, _ptr(out_tok), _ptr(slot), _ptr(slot_tok),
+            _ptr(hist), hist.stride(0) if hist is not None else 0, _ptr(hist_pos),
+            _stream(stream)),
+        "cortex_argmax_partials",
     )
 
 

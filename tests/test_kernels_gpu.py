@@ -461,9 +461,9 @@ def test_paged_prefill_attention(cuda, group, impl):
 # ---------------------------------------------------------------- elementwise
 
 
-def test_rmsnorm_embed_swiglu_argmax(cuda):
+def test_rmsnorm_embed_argmax(cuda):
     o = ops()
-    d, V, T, F = 4096, 1000, 37, 1536
+    d, V, T = 4096, 1000, 37
     g = torch.Generator(device=cuda).manual_seed(1)
     emb = torch.randn(V, d, generator=g, device=cuda).to(torch.bfloat16)
     toks = torch.randint(0, V, (T,), generator=g, device=cuda, dtype=torch.int32)
@@ -479,11 +479,6 @@ def test_rmsnorm_embed_swiglu_argmax(cuda):
     y3 = torch.empty(3, d, device=cuda, dtype=torch.bfloat16)
     o.rmsnorm(h, w, 3, y3, 1e-5, rows=rows)
     assert torch.equal(y3, y[rows.long()])
-    gu = torch.randn(T, 2 * F, generator=g, device=cuda).to(torch.bfloat16)
-    act = torch.empty(T, F, device=cuda, dtype=torch.bfloat16)
-    o.swiglu(gu, T, act)
-    gg, uu = gu[:, :F].float(), gu[:, F:].float()
-    assert rel(act, bf16(gg / (1 + torch.exp(-gg)) * uu)) < 1e-3
     logits = torch.randn(T, 128256, generator=g, device=cuda)
     logits[3, 77] = 100.0
     logits[3, 99] = 100.0  # tie -> first index
@@ -646,3 +641,85 @@ def test_kv_double_free_flagged(cuda):
     o.kv_free(bitmap, 64, 0, table, zero, zero, one * 4, 1, status)
     torch.cuda.synchronize()
     assert int(status[0]) == -1
+
+
+@pytest.mark.parametrize("M,N", [(5, 128256), (129, 128256), (212, 128256), (300, 1024),
+                                 (64, 1024)])
+def test_lm_head_argmax_epilogue(cuda, M, N):
+    """Greedy tokens from the lm_head GEMM's argmax epilogue (out mode 3: (max, index) per
+    128-column chunk, then cortex_argmax_partials) equal the argmax over the full logits of
+    the same GEMM, including exact ties across chunks (first index wins) and a row with no
+    finite logit (token 0)."""
+    o = ops()
+    K = 4096 if N > 1024 else 256
+    g = torch.Generator(device=cuda).manual_seed(M + N)
+    x = torch.randn(max(M, 32), K, generator=g, device=cuda).to(torch.bfloat16)
+    w = (torch.randn(N, K, generator=g, device=cuda) * 0.02).to(torch.bfloat16)
+    w[N - 130] = w[7]  # identical rows in different chunks: exact ties, first index wins
+    w[N - 1] = w[7]
+    x[1] = 0  # a row of zero logits everywhere: the argmax is index 0
+    if M > 3:
+        x[3, 0] = float("nan")  # NaN logits in every column: token 0
+    ws = o.GemmWorkspace(cuda)
+    logits = torch.empty(M, N, device=cuda)
+    o.gemm(o.weight_map(w), o.act_map(x), M, logits, ws)
+    want = torch.empty(M, dtype=torch.int32, device=cuda)
+    o.argmax(logits, M, N, out_tok=want)
+    part = torch.empty(M, N // 128, dtype=torch.int64, device=cuda)
+    o.gemm(o.weight_map(w), o.act_map(x), M, part, ws, argmax=True)
+    got = torch.empty(M, dtype=torch.int32, device=cuda)
+    o.argmax_partials(part, M, out_tok=got)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+    assert int(got[1]) == 0
+    if M > 3:
+        assert int(got[3]) == 0
+    ties = (logits[:, 7] == logits.max(dim=1).values).nonzero().flatten()
+    assert all(int(got[r]) == 7 for r in ties.tolist() if r not in (1, 3))
+
+
+@pytest.mark.parametrize("mode", [0, 2])
+@pytest.mark.parametrize("M,hq,hkv,K", [(5, 32, 8, 4096), (129, 32, 8, 4096), (200, 32, 8, 4096),
+                                        (700, 32, 8, 4096), (300, 2, 1, 256), (40, 16, 4, 4096)])
+def test_gemm_qkv_rope_epilogue(cuda, mode, M, hq, hkv, K):
+    """The QKV GEMM with RoPE + paged KV append in its epilogue (every GEMM path: automatic
+    plan = split-K / 2-SM by M, forced 2-SM) against the unfused GEMM + rope_kv_append."""
+    o = ops()
+    N = (hq + 2 * hkv) * 128
+    nb = 256
+    g = torch.Generator(device=cuda).manual_seed(M + hq)
+    x = torch.randn(max(M, 32), K, generator=g, device=cuda).to(torch.bfloat16)
+    w = (torch.randn(N, K, generator=g, device=cuda) * 0.05).to(torch.bfloat16)
+    table = torch.randperm(nb * 4, generator=torch.Generator().manual_seed(M))[:nb].to(
+        torch.int32).view(8, 32).to(cuda) % nb
+    rng = np.random.default_rng(M)
+    # distinct (row, col, off) slots per token
+    slots = rng.permutation(8 * 32 * 16)[:M]
+    rows = torch.as_tensor(slots // (32 * 16), dtype=torch.int32, device=cuda)
+    cols = torch.as_tensor((slots // 16) % 32, dtype=torch.int32, device=cuda)
+    offs = torch.as_tensor(slots % 16, dtype=torch.int32, device=cuda)
+    table = torch.arange(8 * 32, dtype=torch.int32, device=cuda).view(8, 32)  # distinct blocks
+    pos = torch.as_tensor(rng.integers(0, 8000, M), dtype=torch.int32, device=cuda)
+    cos, sin = rope_tables(8192, 500000.0)
+    cos, sin = cos.to(cuda), sin.to(cuda)
+    ws = o.GemmWorkspace(cuda)
+    k0, v0 = _rows(0, nb, hkv)
+    prev = o.gemm_set_mode(mode)
+    try:
+        qkv = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+        o.gemm(o.weight_map(w), o.act_map(x), M, qkv, ws)
+        q_ref = torch.zeros(M, hq, 128, device=cuda, dtype=torch.bfloat16)
+        c_ref = torch.zeros(1, 2, nb, hkv, 16, 128, device=cuda, dtype=torch.bfloat16)
+        o.rope_kv_append(qkv, q_ref, c_ref, k0, v0, table, pos, rows, cols, offs, cos, sin, M,
+                         hq, hkv)
+        q_got = torch.zeros_like(q_ref)
+        c_got = torch.zeros_like(c_ref)
+        o.gemm_qkv_rope(o.weight_map(w), o.act_map(x), M, ws, q_got, c_got, k0, v0, table, pos,
+                        rows, cols, offs, cos, sin, hq, hkv)
+        torch.cuda.synchronize()
+    finally:
+        o.gemm_set_mode(prev)
+    # same rounding points; only fp32 contraction may differ -> rare 1-ulp bf16 flips
+    for got, ref in ((q_got, q_ref), (c_got, c_ref)):
+        assert rel(got, ref) < 1e-3
+        assert (got != ref).float().mean().item() < 1e-3
