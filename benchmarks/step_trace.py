@@ -33,8 +33,15 @@ def main() -> None:
     ap.add_argument("--json", default=None)
     args = ap.parse_args()
     torch.cuda.set_device(0)
-    rt, cfg, _ = bench.build_runtime("llama3-8b", args.workload, 256, torch.device("cuda", 0), 0, 1)
+    from paper_2510_14126_b200.runtime import PoolRuntime
+
+    spec, _ = bench.workload(args.workload)
+    params = bench.engine_params(spec, 256, 1)
+    worker = bench.build_worker("llama3-8b", spec, [[params, params]], torch.device("cuda", 0))
+    rt = PoolRuntime(worker, spec, params, concurrency=256, prefill_budget=4096 - 512)
     rt.fill()
+    while rt.stats.completed + rt.stats.failed < 256:  # the bench's ramp
+        rt.step()
     rt.run_steps(args.warmup)
     torch.cuda.synchronize()
     # tokens per step (decode + prefill) and the GEMM M it implies

@@ -128,25 +128,26 @@ int32_t cortex_gemm_bf16(const void* tmap_w, const void* tmap_x, int32_t M, int3
 /* QKV projection with RoPE and the paged KV append fused into the GEMM epilogue (the
  * per-token KV write of EngineState.admit's prefill and advance_decode's decode steps,
  * engines.py:142-194): W is [N = (hq + 2 hkv) * 128, K] ([q heads | k heads | v heads]);
- * for token m the accumulators are rounded to bf16, q / k heads rotated (rotate-half,
- * position tok_pos[m], tables cos_tab / sin_tab [max_pos, 64] fp32) and rounded again,
- * q written to q_out [M, hq, 128] and k / v to the token's paged slot (block
- * table[tok_row[m]][tok_col[m]], offset tok_off[m]) of the layer's K / V plane (128-wide
- * rows k_row0 / v_row0 of cache). The qkv activation is never written. */
+ * for token m the accumulators are rounded to bf16, q / k heads rotated (rotate-half)
+ * and rounded again, q written to q_out [M, hq, 128] and k / v to the token's paged slot
+ * of the layer's K / V plane (128-wide rows k_row0 / v_row0 of cache). The qkv
+ * activation is never written. tok_dst / tok_cs come from cortex_rope_token_prep (once
+ * per step): tok_dst[m] = (table[tok_row[m]][tok_col[m]] * hkv) * 16 + tok_off[m], the
+ * token's row within a plane for kv head 0; tok_cs[m] = cos | sin [128] fp32 at
+ * tok_pos[m] (tables [max_pos, 64]). */
 typedef struct {
   void* q_out;
   void* cache;
   int64_t k_row0, v_row0;
-  const int32_t* table;
-  int32_t table_stride;
-  const int32_t* tok_pos;
-  const int32_t* tok_row;
-  const int32_t* tok_col;
-  const int32_t* tok_off;
-  const float* cos_tab;
-  const float* sin_tab;
+  const int32_t* tok_dst;
+  const float* tok_cs;
   int32_t hq, hkv;
 } cortex_rope_epilogue_t;
+int32_t cortex_rope_token_prep(const int32_t* table, int32_t table_stride, const int32_t* tok_pos,
+                               const int32_t* tok_row, const int32_t* tok_col,
+                               const int32_t* tok_off, const float* cos_tab, const float* sin_tab,
+                               int32_t n_tok, int32_t hkv, int32_t* tok_dst, float* tok_cs,
+                               cortex_stream_t stream);
 int32_t cortex_gemm_qkv_rope(const void* tmap_w, const void* tmap_x, int32_t M, int32_t N,
                              int32_t K, const cortex_rope_epilogue_t* epi, float* workspace,
                              uint64_t workspace_bytes, int32_t* counters, int32_t n_counters,

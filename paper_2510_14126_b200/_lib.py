@@ -32,6 +32,7 @@ SIGNATURES: dict[str, list] = {
     "cortex_tmap_encode_2d_bf16": [P, P, U64, U64, U64, ctypes.c_uint32, ctypes.c_uint32],
     "cortex_gemm_bf16": [P, P, I32, I32, I32, P, I32, I32, P, I32, P, U64, P, I32, P],
     "cortex_gemm_qkv_rope": [P, P, I32, I32, I32, P, P, U64, P, I32, P],
+    "cortex_rope_token_prep": [P, I32, P, P, P, P, P, P, I32, I32, P, P, P],
     "cortex_embed": [P, P, P, I32, I32, P, P],
     "cortex_rmsnorm": [P, P, I32, P, I32, F32, P, P],
     "cortex_rope_kv_append": [P, P, P, I64, I64, P, I32, P, P, P, P, P, P, I32, I32, I32, P],
@@ -81,9 +82,8 @@ KNOBS = {name: i for i, name in enumerate(
 class RopeEpilogue(ctypes.Structure):
     """cortex_rope_epilogue_t (include/cortex_b200.h)."""
 
-    _fields_ = [("q_out", P), ("cache", P), ("k_row0", I64), ("v_row0", I64), ("table", P),
-                ("table_stride", I32), ("tok_pos", P), ("tok_row", P), ("tok_col", P),
-                ("tok_off", P), ("cos_tab", P), ("sin_tab", P), ("hq", I32), ("hkv", I32)]
+    _fields_ = [("q_out", P), ("cache", P), ("k_row0", I64), ("v_row0", I64), ("tok_dst", P),
+                ("tok_cs", P), ("hq", I32), ("hkv", I32)]
 
 
 STATUS_NAMES = {0: "ok", -1: "bad argument", -2: "CUDA error", -3: "out of KV blocks",

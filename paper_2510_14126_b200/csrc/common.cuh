@@ -331,40 +331,52 @@ CORTEX_DEVICE uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+CORTEX_DEVICE float round_bf16(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+
 // ---- RoPE + paged KV append in the QKV GEMM's epilogue (out mode 4) ----
 // The QKV projection's 128-column chunks are whole heads ([q heads | k heads | v heads]
 // x 128). For one token row m and head h, lane l holds the fp32 accumulators of dims
 // 4l .. 4l + 3; the epilogue rounds them to bf16 (the unfused path's qkv activation),
 // rotates q / k heads (rotate-half: dim i pairs with i + 64, i.e. lane l with l ^ 16),
 // rounds again and stores q into q_out [T, hq, 128] and k / v straight into the token's
-// paged slot (table[tok_row][tok_col], offset tok_off) of the layer's K / V plane.
+// paged slot of the layer's K / V plane. The per-token operands come from
+// cortex_rope_token_prep (once per step, shared by every layer): tok_dst[m] = the
+// token's 128-wide row within a plane for kv head 0, (block * hkv) * 16 + offset, and
+// tok_cs[m] = cos | sin (64 + 64 fp32) at its position. They are independent loads, so
+// an epilogue issues a chunk's worth of them together with its other global operands.
 struct RopeEpi {
   __nv_bfloat16* q_out;
   __nv_bfloat16* cache;
   int64_t k_row0, v_row0;
-  const int* table;
-  int table_stride;
-  const int* tok_pos;
-  const int* tok_row;
-  const int* tok_col;
-  const int* tok_off;
-  const float* cos_tab;
-  const float* sin_tab;
+  const int* tok_dst;
+  const float* tok_cs;
   int hq, hkv;
 };
 
-CORTEX_DEVICE float round_bf16(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+struct RopeRow {
+  int dst;
+  float4 c, s;
+};
 
-CORTEX_DEVICE void rope_epilogue_row(const RopeEpi& e, int m, int h, float4 v) {
+CORTEX_DEVICE RopeRow rope_fetch(const RopeEpi& e, int m, int h) {
+  RopeRow r;
+  const int i0 = 4 * ((threadIdx.x & 31) & 15);
+  r.dst = 0;
+  r.c = r.s = make_float4(1.f, 1.f, 1.f, 1.f);
+  if (h < e.hq + e.hkv) {
+    r.c = __ldg(reinterpret_cast<const float4*>(e.tok_cs + static_cast<int64_t>(m) * 128 + i0));
+    r.s = __ldg(reinterpret_cast<const float4*>(e.tok_cs + static_cast<int64_t>(m) * 128 + 64 + i0));
+  }
+  if (h >= e.hq) r.dst = __ldg(e.tok_dst + m);
+  return r;
+}
+
+CORTEX_DEVICE void rope_store_row(const RopeEpi& e, const RopeRow& rr, int m, int h, float4 v) {
   const int lane = threadIdx.x & 31;
   float x[4] = {round_bf16(v.x), round_bf16(v.y), round_bf16(v.z), round_bf16(v.w)};
   float y[4];
   if (h < e.hq + e.hkv) {  // (warp-uniform)
-    const int pos = __ldg(e.tok_pos + m);
-    const int i0 = 4 * (lane & 15);
-    const float4 c = __ldg(reinterpret_cast<const float4*>(e.cos_tab + pos * 64 + i0));
-    const float4 s = __ldg(reinterpret_cast<const float4*>(e.sin_tab + pos * 64 + i0));
-    const float cc[4] = {c.x, c.y, c.z, c.w}, ss[4] = {s.x, s.y, s.z, s.w};
+    const float cc[4] = {rr.c.x, rr.c.y, rr.c.z, rr.c.w}, ss[4] = {rr.s.x, rr.s.y, rr.s.z, rr.s.w};
     const bool upper = lane >= 16;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -379,13 +391,9 @@ CORTEX_DEVICE void rope_epilogue_row(const RopeEpi& e, int m, int h, float4 v) {
   if (h < e.hq) {
     dst = e.q_out + (static_cast<int64_t>(m) * e.hq + h) * 128;
   } else {
-    const int block = __ldg(e.table + static_cast<int64_t>(__ldg(e.tok_row + m)) * e.table_stride +
-                            __ldg(e.tok_col + m));
-    const int off = __ldg(e.tok_off + m);
     const bool is_k = h < e.hq + e.hkv;
     const int kh = is_k ? h - e.hq : h - e.hq - e.hkv;
-    dst = e.cache + ((is_k ? e.k_row0 : e.v_row0) + (static_cast<int64_t>(block) * e.hkv + kh) * 16 +
-                     off) * 128;
+    dst = e.cache + ((is_k ? e.k_row0 : e.v_row0) + rr.dst + kh * 16) * 128;
   }
   uint2 packed;
   packed.x = pack_bf16(y[0], y[1]);

@@ -253,6 +253,33 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int64_t ld, int 
   }
 }
 
+// Per-token operands of the QKV GEMM's RoPE epilogue, once per step (shared by every
+// layer): the token's K / V row within a plane and cos | sin at its position.
+__global__ void rope_token_prep_kernel(const int* __restrict__ table, int table_stride,
+                                       const int* __restrict__ tok_pos,
+                                       const int* __restrict__ tok_row,
+                                       const int* __restrict__ tok_col,
+                                       const int* __restrict__ tok_off,
+                                       const float* __restrict__ cos_tab,
+                                       const float* __restrict__ sin_tab, int n_tok, int hkv,
+                                       int* __restrict__ tok_dst, float* __restrict__ tok_cs) {
+  pdl_wait();
+  pdl_trigger();
+  const int t = blockIdx.x * (blockDim.x / 32) + warp_id();
+  if (t >= n_tok) return;
+  const int lane = lane_id();
+  const int pos = tok_pos[t];
+  // 128 floats: lanes 0-15 copy cos, 16-31 sin, float4 each
+  const float* src = lane < 16 ? cos_tab + static_cast<int64_t>(pos) * 64 + 4 * lane
+                               : sin_tab + static_cast<int64_t>(pos) * 64 + 4 * (lane - 16);
+  reinterpret_cast<float4*>(tok_cs + static_cast<int64_t>(t) * 128)[lane] =
+      *reinterpret_cast<const float4*>(src);
+  if (lane == 0) {
+    const int block = table[static_cast<int64_t>(tok_row[t]) * table_stride + tok_col[t]];
+    tok_dst[t] = (block * hkv) * 16 + tok_off[t];
+  }
+}
+
 // Greedy token per row from the lm_head GEMM's per-128-column partials (out mode 3):
 // (max, first index) over the row's n_chunks partials, chunk order = column order, so
 // the result is the first index of the row maximum, exactly argmax_kernel's.
@@ -355,6 +382,22 @@ int32_t cortex_rope_kv_append(const void* qkv, void* q_out, void* cache, int64_t
   a.hq = hq;
   a.hkv = hkv;
   if (pdl_launch(rope_kv_append_kernel, n_tok, 256, 0, stream, 1, a) != cudaSuccess)
+    return CORTEX_ECUDA;
+  return CORTEX_OK;
+}
+
+int32_t cortex_rope_token_prep(const int32_t* table, int32_t table_stride, const int32_t* tok_pos,
+                               const int32_t* tok_row, const int32_t* tok_col,
+                               const int32_t* tok_off, const float* cos_tab, const float* sin_tab,
+                               int32_t n_tok, int32_t hkv, int32_t* tok_dst, float* tok_cs,
+                               cudaStream_t stream) {
+  if (!table || !tok_pos || !tok_row || !tok_col || !tok_off || !cos_tab || !sin_tab ||
+      !tok_dst || !tok_cs || n_tok < 0 || hkv < 1)
+    return CORTEX_EBADARG;
+  if (n_tok == 0) return CORTEX_OK;
+  if (pdl_launch(rope_token_prep_kernel, (n_tok + 7) / 8, 256, 0, stream, 1, table, table_stride,
+                 tok_pos, tok_row, tok_col, tok_off, cos_tab, sin_tab, n_tok, hkv, tok_dst,
+                 tok_cs) != cudaSuccess)
     return CORTEX_ECUDA;
   return CORTEX_OK;
 }

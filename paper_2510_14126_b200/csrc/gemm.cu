@@ -55,10 +55,19 @@ struct GemmSmem {
 // four rows' loads are issued before any store (out may alias residual).
 CORTEX_DEVICE void epilogue_rows(const GemmArgs& a, const float* stile, int m0, int rows, int r0,
                                  int lane, int col) {
-  if (a.out_f32 == 4) {  // QKV: the tile's 128 columns are one head
-    for (int r = r0; r < rows; r += 4)
-      rope_epilogue_row(a.rope, m0 + r, (col - 4 * lane) / kBlockN,
-                        reinterpret_cast<const float4*>(stile + r * kBlockN)[lane]);
+  if (a.out_f32 == 4) {  // QKV: the tile's 128 columns are one head; 8 rows' operands at once
+    const int h = (col - 4 * lane) / kBlockN;
+    for (int rb = r0; rb < rows; rb += 32) {
+      RopeRow rr[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (rb + 4 * u < rows) rr[u] = rope_fetch(a.rope, m0 + rb + 4 * u, h);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (rb + 4 * u < rows)
+          rope_store_row(a.rope, rr[u], m0 + rb + 4 * u, h,
+                         reinterpret_cast<const float4*>(stile + (rb + 4 * u) * kBlockN)[lane]);
+    }
     return;
   }
   if (a.out_f32 == 3) {  // greedy-token partials: (max, index) of this tile's 128 columns
@@ -484,8 +493,7 @@ int32_t cortex_gemm_qkv_rope(const void* tmap_w, const void* tmap_x, int32_t M, 
                              int32_t K, const cortex_rope_epilogue_t* epi, float* workspace,
                              uint64_t workspace_bytes, int32_t* counters, int32_t n_counters,
                              cudaStream_t stream) {
-  if (!epi || !epi->q_out || !epi->cache || !epi->table || !epi->tok_pos || !epi->tok_row ||
-      !epi->tok_col || !epi->tok_off || !epi->cos_tab || !epi->sin_tab || epi->hq < 1 ||
+  if (!epi || !epi->q_out || !epi->cache || !epi->tok_dst || !epi->tok_cs || epi->hq < 1 ||
       epi->hkv < 1 || N != (epi->hq + 2 * epi->hkv) * 128)
     return CORTEX_EBADARG;
   RopeEpi r{};
@@ -493,14 +501,8 @@ int32_t cortex_gemm_qkv_rope(const void* tmap_w, const void* tmap_x, int32_t M, 
   r.cache = reinterpret_cast<__nv_bfloat16*>(epi->cache);
   r.k_row0 = epi->k_row0;
   r.v_row0 = epi->v_row0;
-  r.table = epi->table;
-  r.table_stride = epi->table_stride;
-  r.tok_pos = epi->tok_pos;
-  r.tok_row = epi->tok_row;
-  r.tok_col = epi->tok_col;
-  r.tok_off = epi->tok_off;
-  r.cos_tab = epi->cos_tab;
-  r.sin_tab = epi->sin_tab;
+  r.tok_dst = epi->tok_dst;
+  r.tok_cs = epi->tok_cs;
   r.hq = epi->hq;
   r.hkv = epi->hkv;
   return gemm_dispatch(tmap_w, tmap_x, M, N, K, nullptr, 0, 4, nullptr, 0, workspace,

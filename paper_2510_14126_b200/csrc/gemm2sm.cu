@@ -131,14 +131,14 @@ CORTEX_DEVICE void epi_bar_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memor
 // Each warp covers one 128-column row with 16-byte accesses; all loads before any store
 // (out may alias the residual).
 CORTEX_DEVICE void store_chunk(const Gemm2Args& args, const float* staging, int mrow0, int crow,
-                               int ew, int lane, int col) {
+                               int ew, int lane, int col, const RopeRow* rr) {
   if (args.out_f32 == 4) {  // QKV: this CTA's 128 columns are one head
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int r = ew + 4 * q;
       if (r < crow)  // (warp-uniform)
-        rope_epilogue_row(args.rope, mrow0 + r, (col - 4 * lane) / 128,
-                          reinterpret_cast<const float4*>(staging + r * 128)[lane]);
+        rope_store_row(args.rope, rr[q], mrow0 + r, (col - 4 * lane) / 128,
+                       reinterpret_cast<const float4*>(staging + r * 128)[lane]);
     }
     return;
   }
@@ -378,8 +378,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         // global operands of this chunk first (residual, stream-K partials): their round
         // trip overlaps the TMEM read and the staging transpose
         float4 acc[8];
+        RopeRow rr[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (!contrib && args.out_f32 == 4) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (ew + 4 * q < crow) rr[q] = rope_fetch(args.rope, m0 + c0 + ew + 4 * q, n0 / 128);
+        }
         if (!contrib) {
           if (args.residual && args.out_f32 != 2) {
 #pragma unroll
@@ -445,7 +451,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             }
             __syncwarp();
           }
-          store_chunk(args, staging, m0 + c0, crow, ew, lane, col);
+          store_chunk(args, staging, m0 + c0, crow, ew, lane, col, rr);
         } else {
 #pragma unroll
           for (int q = 0; q < 8; ++q) {

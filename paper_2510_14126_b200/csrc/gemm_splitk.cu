@@ -82,10 +82,12 @@ CORTEX_DEVICE void reduce_rows(const SkArgs& args, const float* base, size_t spl
   for (int rb = r_lo + warp_id(); rb < r_hi; rb += nw * kB) {
     float4 p[KS][kB];
     float4 acc[kB];
+    RopeRow rr[kB];
 #pragma unroll
     for (int i = 0; i < kB; ++i) {
       const int r = rb + i * nw;
       acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < r_hi && args.out_f32 == 4) rr[i] = rope_fetch(args.rope, m0 + r, n0 / 128);
       if (r < r_hi) {
 #pragma unroll
         for (int q = 0; q < KS; ++q)
@@ -109,7 +111,7 @@ CORTEX_DEVICE void reduce_rows(const SkArgs& args, const float* base, size_t spl
         sum.w += p[q][i].w;
       }
       if (args.out_f32 == 4) {  // QKV: the 128 columns are one head
-        rope_epilogue_row(args.rope, m0 + r, n0 / 128, sum);
+        rope_store_row(args.rope, rr[i], m0 + r, n0 / 128, sum);
         continue;
       }
       if (swiglu) {  // lanes 0-15 hold gate features, 16-31 the matching ups

@@ -236,6 +236,11 @@ class GpuWorker:
         # `full_logits` is set (parity checks) or an on_forward hook may read them
         self.lm_part = torch.zeros(max_out, cfg.vocab // 128, dtype=torch.int64, device=dev)
         self.full_logits = False
+        # RoPE + paged KV append in the QKV GEMM's epilogue (False: separate kernel; A/B),
+        # its per-token operands computed once per step
+        self.fuse_qkv_rope = True
+        self.tok_dst = torch.zeros(T, dtype=torch.int32, device=dev)
+        self.tok_cs = torch.zeros(T, 128, dtype=torch.float32, device=dev)
         self.out_tok = torch.zeros(max_out, dtype=torch.int32, device=dev)
         self.xn_map = ops.act_map(self.xn)
         self.attn_map = ops.act_map(self.attn)
@@ -609,6 +614,10 @@ class GpuWorker:
                            2.0 * M * N * K)
 
         tp = self.tp
+        if self.fuse_qkv_rope:
+            ops.rope_token_prep(self.table, d_pos, d_arow, d_acol, d_aoff, self.cos, self.sin, T,
+                                hkv, self.tok_dst, self.tok_cs)
+            nl += 1
         for li in range(cfg.n_layers):
             p = f"layers.{li}."
             k0, v0 = self.layer_rows(li)
@@ -617,14 +626,20 @@ class GpuWorker:
                 nl += 1
             # QKV GEMM with RoPE + the paged KV append in its epilogue (the qkv activation
             # is never written)
-            e0 = prof.open("gemm") if prof is not None else None
-            ops.gemm_qkv_rope(wm[p + "wqkv"], self.xn_map, T, ws, self.q, self.cache, k0, v0,
-                              self.table, d_pos, d_arow, d_acol, d_aoff, self.cos, self.sin, hq,
-                              hkv)
-            if e0 is not None:
-                N, K = wm[p + "wqkv"].rows, wm[p + "wqkv"].cols
-                prof.close("gemm", e0, 2.0 * N * K + 2.0 * T * K + 2.0 * T * N, 2.0 * T * N * K)
-            nl += 1
+            if self.fuse_qkv_rope:
+                e0 = prof.open("gemm") if prof is not None else None
+                ops.gemm_qkv_rope(wm[p + "wqkv"], self.xn_map, T, ws, self.q, self.cache, k0, v0,
+                                  self.tok_dst, self.tok_cs, hq, hkv)
+                if e0 is not None:
+                    N, K = wm[p + "wqkv"].rows, wm[p + "wqkv"].cols
+                    prof.close("gemm", e0, 2.0 * N * K + 2.0 * T * K + 2.0 * T * N,
+                               2.0 * T * N * K)
+                nl += 1
+            else:
+                gemm(p + "wqkv", self.xn_map, T, self.qkv)
+                ops.rope_kv_append(self.qkv, self.q, self.cache, k0, v0, self.table, d_pos,
+                                   d_arow, d_acol, d_aoff, self.cos, self.sin, T, hq, hkv)
+                nl += 2
             def prefill_attn(stream=None):
                 if self.tc_attention:
                     ops.fmha_prefill(self.kvmap, self.qmap, self.attn, self.table, d_prow, d_ppre,

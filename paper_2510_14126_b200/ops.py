@@ -163,17 +163,24 @@ def gemm(wmap: TensorMap, xmap: TensorMap, M: int, out: torch.Tensor, ws: GemmWo
     return out
 
 
+def rope_token_prep(table, tok_pos, tok_row, tok_col, tok_off, cos_tab, sin_tab, n_tok, hkv,
+                    tok_dst, tok_cs, stream=None) -> None:
+    """Per-step operands of gemm_qkv_rope: K/V row within a plane, cos | sin per token."""
+    _check(lib().cortex_rope_token_prep(
+        table.data_ptr(), table.stride(0), tok_pos.data_ptr(), tok_row.data_ptr(),
+        tok_col.data_ptr(), tok_off.data_ptr(), cos_tab.data_ptr(), sin_tab.data_ptr(), n_tok,
+        hkv, tok_dst.data_ptr(), tok_cs.data_ptr(), _stream(stream)), "cortex_rope_token_prep")
+
+
 def gemm_qkv_rope(wmap: TensorMap, xmap: TensorMap, M: int, ws: GemmWorkspace, q_out, cache,
-                  k_row0, v_row0, table, tok_pos, tok_row, tok_col, tok_off, cos_tab, sin_tab,
-                  hq: int, hkv: int, stream=None) -> None:
-    """QKV projection with RoPE + paged KV append in the epilogue (rope_kv_append fused)."""
+                  k_row0, v_row0, tok_dst, tok_cs, hq: int, hkv: int, stream=None) -> None:
+    """QKV projection with RoPE + paged KV append in the epilogue (rope_kv_append fused);
+    tok_dst / tok_cs from rope_token_prep."""
     N, K = wmap.rows, wmap.cols
     if xmap.cols != K or M > xmap.rows or N != (hq + 2 * hkv) * 128:
         raise ValueError("qkv gemm shape mismatch")
-    e = _lib.RopeEpilogue(q_out.data_ptr(), cache.data_ptr(), k_row0, v_row0, table.data_ptr(),
-                          table.stride(0), tok_pos.data_ptr(), tok_row.data_ptr(),
-                          tok_col.data_ptr(), tok_off.data_ptr(), cos_tab.data_ptr(),
-                          sin_tab.data_ptr(), hq, hkv)
+    e = _lib.RopeEpilogue(q_out.data_ptr(), cache.data_ptr(), k_row0, v_row0, tok_dst.data_ptr(),
+                          tok_cs.data_ptr(), hq, hkv)
     _check(lib().cortex_gemm_qkv_rope(wmap.ptr, xmap.ptr, M, N, K, ctypes.byref(e),
                                       ws.ws.data_ptr(), ws.ws.numel() * 4,
                                       ws.counters.data_ptr(), ws.counters.numel(),

@@ -714,8 +714,11 @@ def test_gemm_qkv_rope_epilogue(cuda, mode, M, hq, hkv, K):
                          hq, hkv)
         q_got = torch.zeros_like(q_ref)
         c_got = torch.zeros_like(c_ref)
-        o.gemm_qkv_rope(o.weight_map(w), o.act_map(x), M, ws, q_got, c_got, k0, v0, table, pos,
-                        rows, cols, offs, cos, sin, hq, hkv)
+        tok_dst = torch.empty(M, dtype=torch.int32, device=cuda)
+        tok_cs = torch.empty(M, 128, device=cuda)
+        o.rope_token_prep(table, pos, rows, cols, offs, cos, sin, M, hkv, tok_dst, tok_cs)
+        o.gemm_qkv_rope(o.weight_map(w), o.act_map(x), M, ws, q_got, c_got, k0, v0, tok_dst,
+                        tok_cs, hq, hkv)
         torch.cuda.synchronize()
     finally:
         o.gemm_set_mode(prev)

@@ -27,6 +27,7 @@ def prompts(vocab: int) -> list[np.ndarray]:
 def make_worker(cfg, device, weights, tp=None) -> GpuWorker:
     w = GpuWorker(cfg, device, N_BLOCKS, ROWS, COLS, max_tokens=MAX_TOKENS, max_out=MAX_OUT,
                   hist_cols=HIST, max_seq_tokens=MAX_SEQ, weights=weights, tp=tp)
+    w.full_logits = True  # the tests compare every step's logits
     perm = torch.randperm(N_BLOCKS, generator=torch.Generator().manual_seed(5)).to(torch.int32)
     w.table.copy_(perm.view(ROWS, COLS).to(w.device))
     return w

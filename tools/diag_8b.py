@@ -43,6 +43,7 @@ def main():
     nb = 200
     w = GpuWorker(cfg, dev, n_blocks=nb, n_rows=8, row_cols=nb, max_tokens=2048, max_out=16,
                   hist_cols=64, max_seq_tokens=1400)
+    w.full_logits = True
     # row 0 = prefix (blocks 0..62), row 1 = call (prefix blocks then private blocks)
     npb = (P + 15) // 16
     w.table[0, :npb] = torch.arange(npb, dtype=torch.int32)
