@@ -426,12 +426,12 @@ def run_arm(args, arm, worker, cfg, desc, barrier, all_reduce, device, local, n_
           worker.launches, worker.h2d_bytes, st.d2h_bytes)
     kv_samples = []
     clocks.start()
-    # CORTEX_NCU_TIMED=1: open the profiler range on exactly the timed steps, so an
-    # `ncu --profile-from-start off` launch list describes the same step mix as `value`
+    # CORTEX_NCU_TIMED=1: an NVTX range "timed" around exactly the timed steps, so an
+    # `ncu --nvtx --nvtx-include timed/` launch list describes the same step mix as `value`
     # (profiles/traffic.json -> roofline.traffic)
     ncu_window = timed and os.environ.get("CORTEX_NCU_TIMED") == "1"
     if ncu_window:
-        torch.cuda.profiler.start()
+        torch.cuda.nvtx.range_push("timed")
     t_wall0 = time.perf_counter()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -447,7 +447,7 @@ def run_arm(args, arm, worker, cfg, desc, barrier, all_reduce, device, local, n_
     torch.cuda.synchronize()
     t_wall = time.perf_counter() - t_wall0
     if ncu_window:
-        torch.cuda.profiler.stop()
+        torch.cuda.nvtx.range_pop()
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
     t = torch.tensor([ms, t_wall * 1e3], device=device)

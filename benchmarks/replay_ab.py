@@ -109,10 +109,6 @@ def main() -> None:
                 print(f"  {name[:64]:64s} {n:7.1f} launches {ms:8.3f} ms {100 * ms / tot:5.1f}%")
 
 
-if __name__ == "__main__":
-    main()
-
-
 def kernel_table(w, plans, n_rep: int = 2) -> list:
     """Per-kernel device time (CUPTI) of replaying `plans` with PDL off (so a kernel's
     duration is its own execution, not its early launch waiting on the predecessor)."""
@@ -140,3 +136,8 @@ def kernel_table(w, plans, n_rep: int = 2) -> list:
         per[name][1] += (ev.time_range.end - ev.time_range.start) / 1e3
     steps = n_rep * len(plans)
     return sorted(((k, n / steps, ms / steps) for k, (n, ms) in per.items()), key=lambda r: -r[2])
+
+
+if __name__ == "__main__":
+    main()
+

@@ -189,6 +189,28 @@ CORTEX_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Cross-CTA flags in global memory (split-K publication): release store / acquire spin.
+CORTEX_DEVICE void st_release_gpu_u32(int* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+// Spin until *p == v (acquire, gpu scope); a flag that never arrives (~9 s of SM clock)
+// traps with a diagnostic instead of hanging the GPU.
+CORTEX_DEVICE void wait_flag_gpu(const int* p, uint32_t v) {
+  const long long t0 = clock64();
+  while (true) {
+    uint32_t x;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(x) : "l"(p) : "memory");
+    if (x == v) return;
+    __nanosleep(32);
+    if (clock64() - t0 > (16ll << 30)) {
+      printf("cortex flag hang: grid %d block %d thread %d want %u have %u\n", gridDim.x,
+             blockIdx.x, threadIdx.x, v, x);
+      __trap();
+    }
+  }
+}
+
 // --------------------------------------------------------------------------
 // TMA (cp.async.bulk.tensor) and 1D bulk copies
 

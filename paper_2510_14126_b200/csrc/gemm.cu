@@ -337,6 +337,7 @@ extern "C" int32_t cortex_gemm_splitk_launch(const void* tmap_w, const void* tma
                                              int32_t N, int32_t K, void* out, int32_t ldo,
                                              int32_t out_f32, const void* residual, int32_t ldr,
                                              float* workspace, uint64_t workspace_bytes,
+                                             int32_t* counters, int32_t n_counters,
                                              const RopeEpi* rope, cudaStream_t stream);
 
 extern "C" {
@@ -434,7 +435,8 @@ static int32_t gemm_dispatch(const void* tmap_w, const void* tmap_x, int32_t M, 
   if (out_f32 == 3 && path == 3) path = M > 128 ? 2 : 1;  // (lm_head never plans split-K)
   if (path == 3)
     return cortex_gemm_splitk_launch(tmap_w, tmap_x, M, N, K, out, ldo, out_f32, residual, ldr,
-                                     workspace, workspace_bytes, rope, stream);
+                                     workspace, workspace_bytes, counters, n_counters, rope,
+                                     stream);
   if (path == 2)
     return cortex_gemm_2sm_launch(tmap_w, tmap_x, M, N, K, out, ldo, out_f32, residual, ldr,
                                   workspace, workspace_bytes, counters, n_counters, rope, stream);

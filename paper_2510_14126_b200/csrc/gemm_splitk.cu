@@ -1,4 +1,5 @@
-// Decode-sized projections: 2-SM tcgen05 GEMM, split-K over a cluster of CTA pairs.
+// Decode-sized projections: 2-SM tcgen05 GEMM, split-K over CTA pairs synchronised
+// through global flags.
 //
 //   C[m, n] = sum_k X[m, k] * W[n, k]        (+ residual[m, n], fp32)
 //
@@ -11,13 +12,18 @@
 //     rows (cta_group::2, M = 256), which keeps the activation share of every CTA's
 //     TMA ingest low;
 //   * the N = 4096 / 6144 projections have too few 256-row tiles (16 / 24) to occupy
-//     148 SMs, so each tile's K range is split over `ks` pairs that form one cluster
-//     (2 * ks CTAs): the cluster is co-scheduled, so the split partials can be reduced
-//     right away. Every CTA writes its fp32 partial [TN tokens][128 rows] to a
-//     workspace slot, the cluster barrier (release / acquire) publishes them, and then
-//     the pair of split s reduces token rows [s * R, (s + 1) * R) of the tile over all
+//     148 SMs, so each tile's K range is split over `ks` pairs, up to 74 pairs (148
+//     CTAs) in one wave. Every CTA writes its fp32 partial [TN tokens][128 rows] to a
+//     workspace slot and publishes it with a release store of the launch's epoch into
+//     its flag; then the pair of split s waits (acquire) for the flags of the tile's
+//     other splits and reduces token rows [s * R, (s + 1) * R) of the tile over all
 //     splits in split order (deterministic), adds the residual and stores — the
-//     reduction is spread over all CTAs instead of serialised on one.
+//     reduction is spread over all CTAs instead of serialised on one. (The first
+//     version synchronised the splits with a cluster barrier, clusters of 2 ks CTAs:
+//     the GPCs hold only 16 clusters of 6 / 37 of 4, so qkv / o / down ran on 96 of
+//     148 SMs; with flags every pair is an independent 2-CTA cluster.) All pairs of a
+//     launch are co-resident (grid <= 148 CTAs, one per SM), so a waiting CTA never
+//     keeps a producer from being scheduled.
 #include <algorithm>
 #include <cstdlib>
 
@@ -42,6 +48,8 @@ struct SkArgs {
   int kb_per;   // K blocks per split
   int m_tiles;
   float* ws;    // [tiles][ks][2][TN][128] fp32 partials
+  int* flags;   // [tiles][ks][2] split-published flags (epoch values)
+  uint32_t epoch;  // this launch's flag value (strictly increasing per launch)
   int n_issue;  // TMA issuing threads: 1, 2 (weights | tokens) or 4 (two of each)
   int l2pf;     // weight K blocks prefetched into L2 beyond the stages, before the PDL wait
   RopeEpi rope;  // out mode 4 (QKV: RoPE + paged KV append in the epilogue)
@@ -177,11 +185,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + STAGES;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tfull + 1);
 
-  const uint32_t crank = cluster_rank();
-  const uint32_t rank = crank & 1u;    // CTA within the pair
-  const uint32_t lead = crank & ~1u;   // the pair leader's cluster rank
-  const int split = static_cast<int>(crank >> 1);
-  const int tile = static_cast<int>(cluster_id_x());
+  const uint32_t rank = cluster_rank();  // CTA within the pair (the cluster)
+  const uint32_t lead = 0;               // the pair leader's cluster rank
+  const int pair_id = static_cast<int>(blockIdx.x >> 1);
+  const int split = pair_id % args.ks;
+  const int tile = pair_id / args.ks;
   const int n_tile = tile / args.m_tiles;
   const int m_tile = tile % args.m_tiles;
   const int total_kb = args.K / kBK;
@@ -324,12 +332,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
-  // every split's partial is in the workspace before any pair reduces (cluster scope)
+  // every split's partial is in the workspace before any pair reduces: publish this
+  // CTA's partial (release, gpu scope, after the CTA barrier), then acquire the other
+  // splits' flags for this rank's 128 columns
   SK_TRACE(3);
   tc_fence_before();
-  __syncwarp();
-  cluster_arrive_release();
-  cluster_wait_acquire();
+  __syncthreads();
+  int* tflags = args.flags + static_cast<size_t>(tile) * args.ks * 2;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release_gpu_u32(tflags + split * 2 + rank, args.epoch);
+  }
+  if (threadIdx.x < args.ks && static_cast<int>(threadIdx.x) != split)
+    wait_flag_gpu(tflags + threadIdx.x * 2 + rank, args.epoch);
+  __syncthreads();
   SK_TRACE(4);
 
   {
@@ -372,7 +388,7 @@ int32_t launch_sk(const CUtensorMap* tw, const CUtensorMap* tx, const SkArgs& a,
       return CORTEX_ECUDA;
     configured = true;
   }
-  if (pdl_launch(kern, n_clusters * 2 * a.ks, kThreads, L::kTotal, stream, 2 * a.ks, *tw, *tx, a) !=
+  if (pdl_launch(kern, n_clusters * 2 * a.ks, kThreads, L::kTotal, stream, 2, *tw, *tx, a) !=
       cudaSuccess)
     return CORTEX_ECUDA;
   return CORTEX_OK;
@@ -387,10 +403,9 @@ extern "C" {
 // kernel. The split count depends on N and K only, so within the regime a token's result
 // does not depend on the batch it is in (the K split points are fixed; the tile width
 // does not change a dot product's summation order):
-//   * tiles x ks pairs must run as one co-scheduled wave: clusters of 6 CTAs (ks = 3)
-//     fit 16 at a time, clusters of 4 (ks = 2) 37 (measured: qkv with 24 clusters of 6
-//     takes two waves, 1.5x slower);
-//   * ks = 3 where it fits (o / down: 16 tiles -> 48 pairs), else 2 (qkv: 24 -> 48);
+//   * tiles x ks pairs must run as one co-resident wave (<= 74 pairs, 148 CTAs): the
+//     largest ks <= 4 that fits (o / down: 16 tiles -> ks 4, 64 pairs; qkv: 24 -> ks 3,
+//     72 pairs);
 //   * the fp32 partials (ks x M x N x 4 bytes) must stay small next to the weights.
 // Measured at M = 16 ... 256 (benchmarks/gemm_sk_sweep.py): 0.7-0.85x the time of the
 // whole-tile 2-SM kernel for o / down / qkv, 0.45-0.6x the 1-SM split-K kernel.
@@ -411,7 +426,8 @@ int32_t cortex_gemm_splitk_plan(int32_t M, int32_t N, int32_t K, int32_t* tn_out
     ks = g_sk_ks_force;
     if (tiles * mt * ks > 74) return 0;
   } else {
-    ks = tiles * mt * 3 <= 48 ? 3 : (tiles * mt * 2 <= 74 ? 2 : 0);
+    ks = 4;
+    while (ks >= 2 && tiles * mt * ks > 74) --ks;
     while (ks >= 2 && 2 * ks * tn * mt > K) --ks;  // partials <= weights / 2
     if (ks < 2) ks = 0;
     // (wide projections such as gate_up - 112 tiles - stay on the persistent 2-SM kernel:
@@ -432,11 +448,12 @@ int32_t cortex_gemm_splitk_plan(int32_t M, int32_t N, int32_t K, int32_t* tn_out
 int32_t cortex_gemm_splitk_launch(const void* tmap_w, const void* tmap_x, int32_t M, int32_t N,
                                   int32_t K, void* out, int32_t ldo, int32_t out_f32,
                                   const void* residual, int32_t ldr, float* workspace,
-                                  uint64_t workspace_bytes, const RopeEpi* rope,
-                                  cudaStream_t stream) {
+                                  uint64_t workspace_bytes, int32_t* counters,
+                                  int32_t n_counters, const RopeEpi* rope, cudaStream_t stream) {
   int tn = 0, mt = 1, nw = 1;
   const int ks = cortex_gemm_splitk_plan(M, N, K, &tn, &mt, &nw);
-  if (ks < 1 || !workspace || (out_f32 == 4 && !rope)) return CORTEX_EBADARG;
+  if (ks < 1 || !workspace || !counters || n_counters < 1024 || (out_f32 == 4 && !rope))
+    return CORTEX_EBADARG;
   const int total_kb = K / kBK;
   const int tiles = N / (kPairN * nw) * mt;
   if (workspace_bytes < static_cast<uint64_t>(tiles) * ks * 2 * nw * tn * 128 * sizeof(float))
@@ -454,6 +471,13 @@ int32_t cortex_gemm_splitk_launch(const void* tmap_w, const void* tmap_x, int32_
   a.kb_per = (total_kb + ks - 1) / ks;
   a.m_tiles = mt;
   a.ws = workspace;
+  // split flags: the last 512 counters (the 1-SM kernel's tile counters use the first
+  // n_tiles); a strictly increasing epoch per launch means they never need resetting
+  static uint32_t epoch = 0;
+  epoch = epoch == 0x7fffffffu ? 1u : epoch + 1u;
+  a.flags = counters + (n_counters - 512);
+  a.epoch = epoch;
+  if (tiles * ks * 2 > 512) return CORTEX_EBADARG;
   // TMA issuers (knob SK_ISSUE, default 2: 1, 2 and 4 issuers measured within noise of
   // each other at M = 64 ... 256 - the decode GEMMs are bound by L2 throughput, weights
   // plus the token rows every weight tile re-reads, not by TMA issue)

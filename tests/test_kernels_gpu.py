@@ -54,7 +54,8 @@ def test_gemm_matches_fp32(cuda, M, N, K):
     torch.cuda.synchronize()
     assert torch.isfinite(out.float()).all()
     assert rel(out, ref) < 4e-3
-    assert int(ws.counters.abs().sum()) == 0  # split-K counters left zeroed
+    # split-K tile counters left zeroed (the last 512 hold the split flags: epoch values)
+    assert int(ws.counters[:-512].abs().sum()) == 0
 
 
 @pytest.mark.parametrize("M", [3, 64, 257])
@@ -103,7 +104,7 @@ def test_gemm_paths_match(cuda, mode, M, N, K):
         out32 = torch.empty(M, N, device=cuda)
         o.gemm(o.weight_map(w), o.act_map(x), M, out32, ws, residual=r)
         torch.cuda.synchronize()
-        assert int(ws.counters.abs().sum()) == 0  # stream-K flags left zeroed
+        assert int(ws.counters[:-512].abs().sum()) == 0  # stream-K flags left zeroed
     finally:
         _set_gemm_mode(o, 0)
     ref = x[:M].float() @ w.float().T
