@@ -266,17 +266,33 @@ def main() -> None:
         return
 
     dist = None
+    # one process per GPU over NCCL; with fewer GPUs than ranks (a functional check of the
+    # multi-replica path on a 1-GPU box) the ranks share devices over gloo, with
+    # programmatic dependent launch off (ranks time-sliced on one GPU)
+    shared = world > torch.cuda.device_count()
+    if shared:
+        local %= torch.cuda.device_count()
+        from paper_2510_14126_b200 import _lib
+
+        _lib.set_knob("PDL", 0)
     if world > 1:
         dist = tdist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
+    red_dev = torch.device("cpu") if shared else device  # where the reductions run
 
     from paper_2510_14126_b200.cluster import parse_split, plan_engines
 
     tp = args.tp
     if world % tp:
         raise SystemExit("--tp must divide the number of ranks")
+    if tp > 1 and shared:
+        raise SystemExit("--tp 2 needs one GPU per rank (the in-kernel peer exchange); the "
+                         "shared-GPU TP path is covered by tests/test_tp_gpu.py")
     replica, n_rep, tp_rank = rank // tp, world // tp, rank % tp
     # weak scaling: 256 workflows per GPU; an engine's batch cap admits the whole closed
     # loop of its GPU at N = 1 (two engines share it) and twice that alone on a replica
@@ -303,7 +319,7 @@ def main() -> None:
                           tp_comm=tp_comm)
     cfg = worker.full_cfg
     if tp_rank:
-        _follow(worker, tp_ring, dist, device, tp_comm, arms, args, spec, n_rep, replica,
+        _follow(worker, tp_ring, dist, red_dev, tp_comm, arms, args, spec, n_rep, replica,
                 tp_rank, conc_total, max_batch)
         return
     if tp_ring is not None:
@@ -331,7 +347,7 @@ def main() -> None:
             worker.collective("arm")  # the follower joins the arm's link set-up collectives
         arm = Arm(args, mode, spec, worker, n_rep, replica, tp_rank, dist, conc_total,
                   max_batch)
-        res = run_arm(args, arm, worker, cfg, desc, barrier, all_reduce, device, local, n_rep,
+        res = run_arm(args, arm, worker, cfg, desc, barrier, all_reduce, red_dev, local, n_rep,
                       world, timed=ai == 0)
         arm.close()
         if ai == 0:
@@ -346,6 +362,9 @@ def main() -> None:
                                 "control_path": cb["control_path"],
                                 "decode_tok_s": cb["decode_tok_s"]}
     if rank == 0:
+        if shared:
+            line["config"]["functional_only"] = (
+                f"{world} ranks on {torch.cuda.device_count()} GPU(s) over gloo: not a measurement")
         print(json.dumps(line), flush=True)
     if dist is not None:
         if tp_ring is not None:
@@ -414,10 +433,13 @@ def run_arm(args, arm, worker, cfg, desc, barrier, all_reduce, device, local, n_
 
     # ---------------- timed region ----------------
     peaks, peak_src = _peaks()
+    ncu_window = timed and os.environ.get("CORTEX_NCU_TIMED") == "1"
     if rt is not None and timed:
         # the dominant kernel class timed with CUDA events inside the timed steps (every
-        # 8th step instrumented: ~0.7 % event overhead)
-        worker.prof = KernelProfile([dominant], every=8)
+        # 8th step instrumented: ~0.7 % event overhead); under the ncu capture every step,
+        # so the algorithmic bytes of exactly the captured launches are known
+        worker.prof = KernelProfile([dominant, "attn_decode_ctx"] if ncu_window else [dominant],
+                                    every=1 if ncu_window else 8)
     clocks = ClockSampler(local)
     barrier()
     torch.cuda.synchronize()
@@ -427,9 +449,9 @@ def run_arm(args, arm, worker, cfg, desc, barrier, all_reduce, device, local, n_
     kv_samples = []
     clocks.start()
     # CORTEX_NCU_TIMED=1: an NVTX range "timed" around exactly the timed steps, so an
-    # `ncu --nvtx --nvtx-include timed/` launch list describes the same step mix as `value`
-    # (profiles/traffic.json -> roofline.traffic)
-    ncu_window = timed and os.environ.get("CORTEX_NCU_TIMED") == "1"
+    # `ncu --nvtx --nvtx-include timed/` launch list describes the same launches whose
+    # algorithmic bytes are written to gpurun_out/ncu_window_algorithmic.json
+    # (tools/ncu_traffic.py -> profiles/traffic.json -> roofline.traffic)
     if ncu_window:
         torch.cuda.nvtx.range_push("timed")
     t_wall0 = time.perf_counter()
@@ -463,8 +485,14 @@ def run_arm(args, arm, worker, cfg, desc, barrier, all_reduce, device, local, n_
     completed, failed, dec_tok, pf_tok, launches, h2d, d2h = [float(x) for x in t]
     kshare = {"launches": 0, "ms": 0.0, "bytes": 0.0, "flops": 0.0}
     if worker.prof is not None:
-        kshare = worker.prof.summary().get(dominant, kshare)
+        summ = worker.prof.summary()
+        kshare = summ.get(dominant, kshare)
         worker.prof = None
+        if ncu_window:
+            os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+            with open(os.path.join(ROOT, "gpurun_out", "ncu_window_algorithmic.json"), "w") as f:
+                json.dump({k: {"launches": v["launches"], "bytes": v["bytes"],
+                               "flops": v["flops"]} for k, v in summ.items()}, f)
     # a kernel-reported error voids the run: no JSON line
     (rt or srv).check_status()
     serve(PHASE_AFTER)
@@ -494,18 +522,22 @@ def run_arm(args, arm, worker, cfg, desc, barrier, all_reduce, device, local, n_
         per_launch = kshare["bytes"] / max(kshare["launches"], 1)
         achieved = kshare["bytes"] / max(kshare["ms"] / 1e3, 1e-12) / 1e9
         peak_note = " copy bandwidth"
-    traffic, traffic_src = None, None
+    traffic, traffic_src, traffic_ratio = None, None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):  # DRAM bytes per launch from the committed ncu launch list
         with open(tpath) as f:
             tj = json.load(f)
-        # only a list captured on this bench's own timed window (same step mix)
+        # only a list captured on this bench's own timed window
         if dominant in tj.get("classes", {}) and tj.get("window") == window_tag(args):
             traffic = tj["classes"][dominant]["dram_bytes_per_launch"]
             traffic_src = tj.get("source")
+            traffic_ratio = tj["classes"][dominant].get("dram_per_algorithmic_byte")
     roofline = {"kernel": dominant, "bound": bound, "achieved": achieved, "peak": peak,
                 "unit": unit, "frac": achieved / peak, "traffic": traffic,
                 "traffic_source": traffic_src,
+                # DRAM bytes / algorithmic bytes over the SAME launches of the captured
+                # window: the re-read factor (the capture's step mix is not this run's)
+                "traffic_per_algorithmic_byte": traffic_ratio,
                 "algorithmic_bytes_per_launch": kshare["bytes"] / max(kshare["launches"], 1),
                 "algorithmic_flops_per_launch": kshare["flops"] / max(kshare["launches"], 1),
                 "per_launch_algorithmic": per_launch,

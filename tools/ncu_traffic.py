@@ -1,6 +1,9 @@
 """DRAM traffic per launch of each bench kernel class from an ncu launch list.
 
-    python tools/ncu_traffic.py LAUNCHES.csv [OUT.json]
+    python tools/ncu_traffic.py LAUNCHES.csv [OUT.json [WINDOW [ALGO.json]]]
+
+ALGO.json (bench.py under CORTEX_NCU_TIMED=1) holds the algorithmic bytes of the same
+launches: each class then also gets dram_per_algorithmic_byte, the re-read factor.
 
 The CSV is `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 --csv --log-file ...` of a bench.py run. Kernel names map to the classes bench.py times
@@ -48,9 +51,9 @@ def per_kernel(path: str) -> dict:
     return launches
 
 
-def summarize(path: str) -> dict:
+def summarize(path: str, window: str | None = None) -> dict:
     launches = per_kernel(path)
-    out = {"source": path, "classes": {}}
+    out = {"source": path, "window": window, "classes": {}}
     for cls, keys in CLASSES.items():
         sel = [d for d in launches.values() if any(k in d["name"] for k in keys)]
         if not sel:
@@ -66,7 +69,15 @@ def summarize(path: str) -> dict:
 
 
 if __name__ == "__main__":
-    res = summarize(sys.argv[1])
+    res = summarize(sys.argv[1], sys.argv[3] if len(sys.argv) > 3 else None)
+    if len(sys.argv) > 4:
+        algo = json.load(open(sys.argv[4]))
+        for cls, v in res["classes"].items():
+            a = algo.get(cls)
+            if a and a["launches"] == v["launches"]:  # the same launches
+                v["algorithmic_bytes_per_launch"] = a["bytes"] / a["launches"]
+                v["dram_per_algorithmic_byte"] = v["dram_bytes_per_launch"] / (
+                    a["bytes"] / a["launches"])
     print(json.dumps(res, indent=1))
     if len(sys.argv) > 2:
         with open(sys.argv[2], "w") as f:
