@@ -759,11 +759,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const uint32_t v_addr = smem_u32(smem + kOffKV2 + s * kKVStage + 2 * kKVHalf);
         const uint32_t p_tmem = tmem + 128 * x + 64 * h;
         const uint32_t o_tmem = tmem + 256 + 128 * x;
+        // P = hi + lo (p_lo): hi in this half's first 32 columns, lo in the next 32
+        for (int part = 0; part < 1 + a.p_lo; ++part) {
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          umma_bf16_ts(o_tmem, p_tmem + 8 * kk,
-                       umma_desc_sw128_mn(v_addr + (4 * h + kk) * 2048, kKVHalf), idesc_pv,
-                       (kt | h | kk) != 0 ? 1u : 0u);
+          for (int kk = 0; kk < 4; ++kk) {
+            umma_bf16_ts(o_tmem, p_tmem + 32 * part + 8 * kk,
+                         umma_desc_sw128_mn(v_addr + (4 * h + kk) * 2048, kKVHalf), idesc_pv,
+                         (kt | h | kk | part) != 0 ? 1u : 0u);
+          }
         }
         umma_commit(&o_ready[x]);
         if (kt == n_kt - 1 && h == 1) umma_commit(&o_done[x]);
@@ -871,14 +874,23 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           tmem_st_wait();
         }
         // p = exp2(s * scale - m); P as bf16 (keys 2c / 2c+1 packed in column c) over the
-        // first 32 columns of this half's S
+        // first 32 columns of this half's S, and with p_lo the residual lo = p - hi over
+        // the next 32 (the PV pass then adds P_hi V + P_lo V)
 #pragma unroll
         for (int i = 0; i < 64; ++i) sv[i] = ex2_approx(fmaf(sv[i], a.scale_log2, -m_use));
         const float lsum = sum64(sv);
-        uint32_t hi[32];
+        if (a.p_lo) {
+          uint32_t hi[32], lo[32];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) hi[c] = pack_bf16(sv[2 * c], sv[2 * c + 1]);
-        tmem_st_x32(tmem_s + lane_off + 64 * h, hi);
+          for (int c = 0; c < 32; ++c) split_bf16(sv[2 * c], sv[2 * c + 1], hi[c], lo[c]);
+          tmem_st_x32(tmem_s + lane_off + 64 * h, hi);
+          tmem_st_x32(tmem_s + lane_off + 64 * h + 32, lo);
+        } else {
+          uint32_t hi[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) hi[c] = pack_bf16(sv[2 * c], sv[2 * c + 1]);
+          tmem_st_x32(tmem_s + lane_off + 64 * h, hi);
+        }
         l_run = l_run * alpha + lsum;
         m_run = m_new;
         tmem_st_wait();
@@ -950,8 +962,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 // rounding of the output alone (<= 1.4e-4 beyond it).
 int fmha_p_lo() { return g_cortex_knob[CORTEX_KNOB_FMHA_PLO]; }
 
-// Kernel choice per launch (knob FMHA_2Q: -1 automatic, 0 one Q tile, 1 two; the two-tile
-// kernel has no hi + lo P, so it serves only with FMHA_PLO = 0). A two-tile CTA costs ~1.55x a one-tile
+// Kernel choice per launch (knob FMHA_2Q: -1 automatic, 0 one Q tile, 1 two). A two-tile CTA costs ~1.55x a one-tile
 // CTA (benchmarks/fmha.py: 8K causal prefill 614 -> 807 TFLOP/s, 8 x 200-token prompts
 // 325 -> 406) but the grid halves, so small grids (decode's cascade pass over a
 // 1000-token prefix: 128 one-tile CTAs, 15 us vs 21 us) stay on one tile per CTA:
@@ -986,7 +997,7 @@ int32_t launch_fmha(const CUtensorMap* tq, const CUtensorMap* tkv, const FmhaArg
       return CORTEX_ECUDA;
     configured = true;
   }
-  if (!a.p_lo && fmha_use_2q(grid)) {
+  if (fmha_use_2q(grid)) {
     dim3 g2((grid.x + 1) / 2, grid.y, grid.z);
     if (pdl_launch(fmha2_tc_kernel, g2, kThreadsTC, kSmemTC2, stream, 1, *tq, *tkv, a) !=
         cudaSuccess)

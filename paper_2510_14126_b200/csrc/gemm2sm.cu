@@ -29,6 +29,11 @@
 #include "common.cuh"
 #include "pair.cuh"
 
+#ifndef CORTEX_G2_DEEP  // one more pipeline stage where shared memory allows (0: the round-1 depths;
+                        // benchmarks/gemm.py: 1-3.5 % faster at M = 204 ... 2048)
+#define CORTEX_G2_DEEP 1
+#endif
+
 namespace {
 
 constexpr int kPairN = 256;  // weight rows per CTA pair (MMA M)
@@ -616,12 +621,12 @@ int32_t cortex_gemm_2sm_launch(const void* tmap_w, const void* tmap_x, int32_t M
   const auto* tw = reinterpret_cast<const CUtensorMap*>(tmap_w);
   const auto* tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
   switch (tn) {
-    case 64: return launch2<64, 8>(tw, tx, a, g_num_sms, stream);
-    case 96: return launch2<96, 8>(tw, tx, a, g_num_sms, stream);
-    case 128: return launch2<128, 7>(tw, tx, a, g_num_sms, stream);
-    case 160: return launch2<160, 7>(tw, tx, a, g_num_sms, stream);
-    case 192: return launch2<192, 6>(tw, tx, a, g_num_sms, stream);
+    case 64: return launch2<64, 8 + 2 * CORTEX_G2_DEEP>(tw, tx, a, g_num_sms, stream);
+    case 96: return launch2<96, 8 + CORTEX_G2_DEEP>(tw, tx, a, g_num_sms, stream);
+    case 128: return launch2<128, 7 + CORTEX_G2_DEEP>(tw, tx, a, g_num_sms, stream);
+    case 160: return launch2<160, 7 + CORTEX_G2_DEEP>(tw, tx, a, g_num_sms, stream);
+    case 192: return launch2<192, 6 + CORTEX_G2_DEEP>(tw, tx, a, g_num_sms, stream);
     case 224: return launch2<224, 6>(tw, tx, a, g_num_sms, stream);
-    default: return launch2<256, 5>(tw, tx, a, g_num_sms, stream);
+    default: return launch2<256, 5 + CORTEX_G2_DEEP>(tw, tx, a, g_num_sms, stream);
   }
 }

@@ -30,6 +30,11 @@
 #include "common.cuh"
 #include "pair.cuh"
 
+#ifndef CORTEX_G2_DEEP  // one more pipeline stage where shared memory allows (0: the round-1 depths;
+                        // benchmarks/gemm.py: 1-3.5 % faster at M = 204 ... 2048)
+#define CORTEX_G2_DEEP 1
+#endif
+
 namespace {
 
 constexpr int kPairN = 256;
@@ -501,10 +506,10 @@ int32_t cortex_gemm_splitk_launch(const void* tmap_w, const void* tmap_x, int32_
     case 64: return launch_sk<64, 8, 1>(tw, tx, a, tiles, stream);
     case 96: return launch_sk<96, 8, 1>(tw, tx, a, tiles, stream);
     case 128: return launch_sk<128, 8, 1>(tw, tx, a, tiles, stream);
-    case 160: return launch_sk<160, 6, 1>(tw, tx, a, tiles, stream);
-    case 192: return launch_sk<192, 6, 1>(tw, tx, a, tiles, stream);
-    case 224: return launch_sk<224, 6, 1>(tw, tx, a, tiles, stream);
-    default: return launch_sk<256, 6, 1>(tw, tx, a, tiles, stream);
+    case 160: return launch_sk<160, 6 + CORTEX_G2_DEEP, 1>(tw, tx, a, tiles, stream);
+    case 192: return launch_sk<192, 6 + CORTEX_G2_DEEP, 1>(tw, tx, a, tiles, stream);
+    case 224: return launch_sk<224, 6 + CORTEX_G2_DEEP, 1>(tw, tx, a, tiles, stream);
+    default: return launch_sk<256, 6 + CORTEX_G2_DEEP, 1>(tw, tx, a, tiles, stream);
   }
 }
 

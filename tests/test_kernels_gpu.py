@@ -396,7 +396,7 @@ def test_cascade_decode_attention(cuda, group, plens, impl):
     from paper_2510_14126_b200 import _lib
 
     o.fmha_set_2q(0 if impl == "tc1" else 1)
-    plo = _lib.set_knob("FMHA_PLO", 1 if impl == "tc1" else 0)  # two tiles: bf16 P only
+    plo = _lib.set_knob("FMHA_PLO", 0 if impl == "tc-bf16p" else 1)
     try:
         o.paged_decode_attn(o.kv_map(cache.view(-1, 128)), q, table, dev(seq_row), dev(seq_pre),
                             dev(seq_kv), B, hkv, group, k0, v0, 1 / math.sqrt(128), o_part,
@@ -414,9 +414,10 @@ def test_cascade_decode_attention(cuda, group, plens, impl):
 
 
 @pytest.mark.parametrize("group", [4, 2])
-@pytest.mark.parametrize("impl", ["mma", "tc", "tc1"])
+@pytest.mark.parametrize("impl", ["mma", "tc", "tc1", "tc-bf16p"])
 def test_paged_prefill_attention(cuda, group, impl):
-    """tc: two-Q-tile tcgen05 kernel (default), tc1: one tile per CTA, mma: mma.sync."""
+    """tc: two-Q-tile tcgen05 kernel, tc1: one tile per CTA (both with P as bf16 hi + lo,
+    the default), tc-bf16p: two tiles with bf16 P alone, mma: mma.sync."""
     o = ops()
     hkv, L, nb, max_blocks = 2, 1, 512, 160
     hq = hkv * group
@@ -444,7 +445,7 @@ def test_paged_prefill_attention(cuda, group, impl):
         from paper_2510_14126_b200 import _lib
 
         o.fmha_set_2q(0 if impl == "tc1" else 1)
-        plo = _lib.set_knob("FMHA_PLO", 1 if impl == "tc1" else 0)  # two tiles: bf16 P
+        plo = _lib.set_knob("FMHA_PLO", 0 if impl == "tc-bf16p" else 1)
         try:
             o.fmha_prefill(kvmap, o.QMap(q, hq, group), out, *args)
         finally:
