@@ -495,7 +495,6 @@ def run_arm(args, arm, worker, cfg, desc, barrier, all_reduce, device, local, n_
                                "flops": v["flops"]} for k, v in summ.items()}, f)
     # a kernel-reported error voids the run: no JSON line
     (rt or srv).check_status()
-    serve(PHASE_AFTER)
     barrier()
     if rt is None:
         return None
