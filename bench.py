@@ -290,9 +290,7 @@ def main() -> None:
     tp = args.tp
     if world % tp:
         raise SystemExit("--tp must divide the number of ranks")
-    if tp > 1 and shared:
-        raise SystemExit("--tp 2 needs one GPU per rank (the in-kernel peer exchange); the "
-                         "shared-GPU TP path is covered by tests/test_tp_gpu.py")
+
     replica, n_rep, tp_rank = rank // tp, world // tp, rank % tp
     # weak scaling: 256 workflows per GPU; an engine's batch cap admits the whole closed
     # loop of its GPU at N = 1 (two engines share it) and twice that alone on a replica
@@ -317,6 +315,15 @@ def main() -> None:
         tp_ring = open_replica_ring(dist, replica, tp_rank)
     worker = build_worker(args.model, spec, [arm_params(m) for m in arms], device,
                           tp_comm=tp_comm)
+    if tp > 1 and shared:
+        # functional TP runs with a replica's two ranks on ONE GPU: every exchange point
+        # waits on the host until both ranks' partials exist (no kernel spins on a rank
+        # that is time-sliced out)
+        def tp_sync(g=groups[replica]):
+            torch.cuda.synchronize()
+            dist.barrier(group=g)
+
+        worker.tp_sync = tp_sync
     cfg = worker.full_cfg
     if tp_rank:
         _follow(worker, tp_ring, dist, red_dev, tp_comm, arms, args, spec, n_rep, replica,

@@ -24,7 +24,13 @@ import bench  # noqa: E402
 
 def main(steps: int = 300) -> None:
     torch.cuda.set_device(0)
-    rt, cfg, _ = bench.build_runtime("llama3-8b", "config2", 256, torch.device("cuda", 0), 0, 1)
+    from paper_2510_14126_b200.runtime import PoolRuntime
+
+    spec, _ = bench.workload("config2")
+    params = bench.engine_params(spec, 256, 1)
+    worker = bench.build_worker("llama3-8b", spec, [[params, params]], torch.device("cuda", 0))
+    rt = PoolRuntime(worker, spec, params, concurrency=256, prefill_budget=4096 - 512)
+    cfg = worker.full_cfg
     w = rt.worker
     rt.fill()
     rt.run_steps(150)

@@ -282,7 +282,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         const int n_tile = g.t / args.m_tiles;
         const int m_tile = g.t % args.m_tiles;
         (void)m_tile;
+#ifdef CORTEX_G2_SAME_A  // (experiment: every pair streams the same weight tile)
+        const int n0 = rank * 128 + 0 * n_tile;
+#else
         const int n0 = n_tile * kPairN + rank * 128;
+#endif
         if (first) {  // the K blocks after the first STAGES: into L2 before the wait
           const int pf1 = min(g.kb1, g.kb0 + STAGES + args.l2pf);
           for (int kb = g.kb0 + STAGES; kb < pf1; ++kb) tma_prefetch_l2_2d(&tmap_w, kb * kBK, n0);
@@ -314,7 +318,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       Seg g;
       while (seg_next(args, pair, pos, g)) {
         const int m_tile = g.t % args.m_tiles;
+#ifdef CORTEX_G2_SAME_B  // (experiment: every pair streams the same token rows)
+        const int x0 = rank * (TN / 2) + 0 * m_tile;
+#else
         const int x0 = m_tile * TN + rank * (TN / 2);
+#endif
         for (int kb = g.kb0; kb < g.kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
