@@ -70,6 +70,7 @@ DEV_SIGNATURES: dict[str, list] = {
     "cortex_gemm2_tile": [I32, I32, I32],
     "cortex_gemm_splitk_plan": [I32, I32, I32, P, P, P],
     "cortex_decode_tiles_per_chunk": [I32, I32],
+    "cortex_act_box_rows": [],
     "cortex_paged_prefill_attn": [P, P, P, P, I32, P, P, P, P, P, I32, I32, I32, I32, I64, I64,
                                   F32, P],
 }
@@ -98,7 +99,7 @@ def load() -> ctypes.CDLL:
     global _LIB
     if _LIB is None:
         # CORTEX_LIB: an alternative build of the same library (tuning variants)
-        path = Path(os.environ.get("CORTEX_LIB", str(LIB_PATH)))
+        path = Path(os.environ.get("CORTEX_LIB") or str(LIB_PATH))
         if not path.exists():
             raise ImportError(
                 f"{path} is missing; build it with `python -m paper_2510_14126_b200.build` "

@@ -18,6 +18,12 @@
 
 #define CORTEX_DEVICE __device__ __forceinline__
 
+// Activation rows per TMA box of the GEMMs' token operand (the host builds the
+// activation tensor maps with cortex_act_box_rows() rows per box).
+#ifndef CORTEX_XBOX
+#define CORTEX_XBOX 16
+#endif
+
 #define CORTEX_BUILDING 1
 #include <cstdio>
 

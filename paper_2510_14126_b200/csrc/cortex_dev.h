@@ -21,7 +21,7 @@ extern "C" {
 enum CortexKnob {
   CORTEX_KNOB_PDL = 0,        /* programmatic dependent launch: 1 on (default), 0 off */
   CORTEX_KNOB_GEMM_MODE,      /* 0 auto, 1 force 1-SM, 2 force 2-SM, 3 prefer cluster split-K */
-  CORTEX_KNOB_GEMM_STREAM_K,  /* 2-SM scheduling: -1 auto, 0 whole tiles, 1 stream-K, 2 hybrid */
+  CORTEX_KNOB_GEMM_STREAM_K,  /* 2-SM scheduling: -1 auto (whole tiles), 0 whole, 1 stream-K */
   CORTEX_KNOB_GEMM_TN,        /* 2-SM token tile width: -1 planner, else 64..256 step 32 */
   CORTEX_KNOB_GEMM_L2PF,      /* weight K blocks prefetched to L2 before the PDL wait (0) */
   CORTEX_KNOB_SK_KS,          /* cluster split-K: splits (-1 planner, 2..4) */
@@ -43,6 +43,7 @@ int32_t cortex_gemm2_tile(int32_t M, int32_t N, int32_t K); /* TN | (stream_k <<
 int32_t cortex_gemm_splitk_plan(int32_t M, int32_t N, int32_t K, int32_t* tn_out,
                                 int32_t* m_tiles_out, int32_t* weight_subtiles_out);
 int32_t cortex_decode_tiles_per_chunk(int32_t total_tiles, int32_t n_kv_heads);
+int32_t cortex_act_box_rows(void); /* token rows per TMA box of the GEMMs' activation maps */
 
 /* mma.sync causal paged prefill attention: the cross-check of cortex_fmha_prefill_tc. */
 int32_t cortex_paged_prefill_attn(const void* tmap_kv, const void* q, void* out,

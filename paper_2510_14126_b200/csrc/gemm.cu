@@ -22,7 +22,7 @@ namespace {
 
 constexpr int kBlockN = 128;  // weight rows per tile (MMA M)
 constexpr int kBlockK = 64;   // K per stage (one 128-byte swizzle row)
-constexpr int kXBox = 16;     // activation rows per TMA box
+constexpr int kXBox = CORTEX_XBOX;  // activation rows per TMA box
 constexpr int kThreads = 128;
 
 struct GemmArgs {
@@ -356,6 +356,9 @@ int32_t cortex_gemm_path(int32_t M, int32_t N, int32_t K) {
   if (mode == 3) return 2;
   return M > 128 ? 2 : 1;
 }
+
+// Rows per TMA box of the activation (token) operand the GEMMs expect.
+int32_t cortex_act_box_rows(void) { return CORTEX_XBOX; }
 
 // Encode a 2-D bf16 TMA descriptor (128 bytes, written to tmap_out) over a
 // row-major matrix [rows, cols] with the given row pitch. box_cols * 2 must be

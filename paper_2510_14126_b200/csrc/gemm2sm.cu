@@ -38,7 +38,7 @@ namespace {
 
 constexpr int kPairN = 256;  // weight rows per CTA pair (MMA M)
 constexpr int kBK = 64;
-constexpr int kXBox2 = 16;   // activation rows per TMA box
+constexpr int kXBox2 = CORTEX_XBOX;  // activation rows per TMA box
 constexpr int kEpiRows = 32; // output rows (m) per epilogue chunk
 constexpr int kThreads2 = 224;  // warps: 0 TMA (weights), 1 MMA, 2-5 epilogue, 6 TMA (tokens)
 struct Gemm2Args {
@@ -51,10 +51,8 @@ struct Gemm2Args {
   int m_tiles;
   int num_tiles;
   int npairs;        // persistent CTA pairs (grid / 2)
-  int sk;            // 0: whole tiles round-robin, 1: stream-K ranges over all tiles,
-                     // 2: hybrid - whole tiles for the full waves, stream-K for the rest
+  int sk;            // 1: stream-K ranges, 0: whole tiles round-robin
   int total_units;   // num_tiles * K blocks
-  int dp_tiles;      // sk == 2: tiles done whole (a multiple of npairs)
   float* workspace;  // stream-K: [npairs * 2][TN][128] fp32 partials
   int* flags;        // stream-K: [npairs * 2] partial-ready flags, left zeroed
   int l2pf;          // weight K blocks prefetched into L2 beyond the stages (first segment)
@@ -65,19 +63,12 @@ struct Seg {
   int t, kb0, kb1;  // tile, K-block range
 };
 
-// First unit of pair p's stream-K range: the units of the tiles not done whole
-// (dp_tiles of them, hybrid mode) split evenly over the pairs.
 CORTEX_DEVICE int sk_begin(const Gemm2Args& a, int p) {
-  const int base = a.dp_tiles * (a.K / kBK);
-  return base + static_cast<int>(static_cast<long long>(p) * (a.total_units - base) / a.npairs);
+  return static_cast<int>(static_cast<long long>(p) * a.total_units / a.npairs);
 }
 
-// Next segment of a pair's work; `pos` starts at seg_start() and is advanced. Hybrid
-// mode encodes the whole-tile phase as pos = -(tile + 1).
-CORTEX_DEVICE int seg_start(const Gemm2Args& a, int pair) {
-  if (a.sk == 2) return pair < a.dp_tiles ? -(pair + 1) : sk_begin(a, pair);
-  return a.sk ? sk_begin(a, pair) : pair;
-}
+// Next segment of a pair's work; `pos` starts at seg_start() and is advanced.
+CORTEX_DEVICE int seg_start(const Gemm2Args& a, int pair) { return a.sk ? sk_begin(a, pair) : pair; }
 
 CORTEX_DEVICE bool seg_next(const Gemm2Args& a, int pair, int& pos, Seg& g) {
   const int tkb = a.K / kBK;
@@ -87,15 +78,6 @@ CORTEX_DEVICE bool seg_next(const Gemm2Args& a, int pair, int& pos, Seg& g) {
     g.kb0 = 0;
     g.kb1 = tkb;
     pos += a.npairs;
-    return true;
-  }
-  if (pos < 0) {  // hybrid: a whole tile of the full waves
-    const int t = -pos - 1;
-    g.t = t;
-    g.kb0 = 0;
-    g.kb1 = tkb;
-    const int nt = t + a.npairs;
-    pos = nt < a.dp_tiles ? -(nt + 1) : sk_begin(a, pair);
     return true;
   }
   const int end = sk_begin(a, pair + 1);
@@ -282,11 +264,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         const int n_tile = g.t / args.m_tiles;
         const int m_tile = g.t % args.m_tiles;
         (void)m_tile;
-#ifdef CORTEX_G2_SAME_A  // (experiment: every pair streams the same weight tile)
-        const int n0 = rank * 128 + 0 * n_tile;
-#else
         const int n0 = n_tile * kPairN + rank * 128;
-#endif
         if (first) {  // the K blocks after the first STAGES: into L2 before the wait
           const int pf1 = min(g.kb1, g.kb0 + STAGES + args.l2pf);
           for (int kb = g.kb0 + STAGES; kb < pf1; ++kb) tma_prefetch_l2_2d(&tmap_w, kb * kBK, n0);
@@ -318,11 +296,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       Seg g;
       while (seg_next(args, pair, pos, g)) {
         const int m_tile = g.t % args.m_tiles;
-#ifdef CORTEX_G2_SAME_B  // (experiment: every pair streams the same token rows)
-        const int x0 = rank * (TN / 2) + 0 * m_tile;
-#else
         const int x0 = m_tile * TN + rank * (TN / 2);
-#endif
         for (int kb = g.kb0; kb < g.kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
@@ -566,42 +540,33 @@ int g_num_sms = 0;
 // (knob GEMM_STREAM_K = 1): it balances the MMA work, but the head pair's fix-up
 // epilogue (reading the partials) measured ~5 us per 32-row chunk at the end of the
 // kernel, so e.g. the down projection at M = 700 takes 107 us vs 73 us in whole tiles
-// (benchmarks/gemm_trace.py with a -DCORTEX_GEMM_TRACE build).
+// (benchmarks/gemm_trace.py with a -DCORTEX_GEMM_TRACE build). A hybrid (whole tiles for
+// the full waves, stream-K for the remainder) measured 17.4 vs 13.2 ms per config-2 step
+// (benchmarks/replay_ab.py) and was removed.
 void cortex_gemm2_plan(int M, int N, int K, int n_sms, int* tn_out, int* sk_out) {
-  // knob GEMM_STREAM_K: -1 automatic (whole tiles or hybrid), 0 whole tiles, 1 stream-K,
-  // 2 hybrid where it applies
-  const int force = g_cortex_knob[CORTEX_KNOB_GEMM_STREAM_K];
+  const int force = g_cortex_knob[CORTEX_KNOB_GEMM_STREAM_K] == 1 ? 1 : 0;
   const int tn_force = g_cortex_knob[CORTEX_KNOB_GEMM_TN];  // tuning: pin the token tile
+  if (tn_force > 0) {
+    *tn_out = tn_force;
+    *sk_out = force;
+    return;
+  }
   const int n_tiles = N / kPairN;
   const int pairs = n_sms / 2;
   double best = -1.0;
   for (int tn : {256, 224, 192, 160, 128, 96, 64}) {
-    if (tn_force > 0 && tn != tn_force) continue;
     const long units = static_cast<long>(n_tiles) * ((M + tn - 1) / tn);
-    for (int sk = 0; sk <= 2; ++sk) {
+    for (int sk = 0; sk <= 1; ++sk) {
       if (force >= 0 && sk != force) continue;
-      if (force < 0 && sk == 1) continue;  // plain stream-K only when forced
       const long waves = (units + pairs - 1) / pairs;
-      double cost;
-      if (sk == 0) {
-        cost = waves * (tn + 32.0);
-      } else if (sk == 1) {
-        cost = static_cast<double>(units) / pairs * (tn + 32.0) * 1.06 + 16.0;
-      } else {
-        const long full = units / pairs, rem = units % pairs;
-        if (full == 0 || rem == 0) continue;  // no full wave / nothing left over
-        cost = full * (tn + 32.0) + static_cast<double>(rem) / pairs * (tn + 32.0) * 1.06 + 16.0;
-      }
+      const double cost = sk ? static_cast<double>(units) / pairs * (tn + 32.0) * 1.06 + 16.0
+                             : waves * (tn + 32.0);
       if (best < 0 || cost < best - 1e-9) {
         best = cost;
         *tn_out = tn;
         *sk_out = sk;
       }
     }
-  }
-  if (best < 0) {  // (a forced mode that does not apply)
-    *tn_out = tn_force > 0 ? tn_force : 256;
-    *sk_out = 0;
   }
 }
 
@@ -651,7 +616,6 @@ int32_t cortex_gemm_2sm_launch(const void* tmap_w, const void* tmap_x, int32_t M
   a.num_tiles = num_tiles;
   a.sk = sk;
   a.total_units = num_tiles * (K / kBK);
-  a.dp_tiles = sk == 2 ? (num_tiles / (g_num_sms / 2)) * (g_num_sms / 2) : 0;
   a.workspace = workspace;
   a.flags = counters;
   a.l2pf = g_cortex_knob[CORTEX_KNOB_GEMM_L2PF];

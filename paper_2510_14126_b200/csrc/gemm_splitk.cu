@@ -39,7 +39,7 @@ namespace {
 
 constexpr int kPairN = 256;
 constexpr int kBK = 64;
-constexpr int kXBox = 16;
+constexpr int kXBox = CORTEX_XBOX;
 constexpr int kThreads = 192;
 
 struct SkArgs {

@@ -230,7 +230,7 @@ bool knob_ok(int knob, int v) {
   switch (knob) {
     case CORTEX_KNOB_PDL: return v == 0 || v == 1;
     case CORTEX_KNOB_GEMM_MODE: return v >= 0 && v <= 3;
-    case CORTEX_KNOB_GEMM_STREAM_K: return v >= -1 && v <= 2;
+    case CORTEX_KNOB_GEMM_STREAM_K: return v >= -1 && v <= 1;
     case CORTEX_KNOB_GEMM_TN: return v == -1 || (v >= 64 && v <= 256 && v % 32 == 0);
     case CORTEX_KNOB_GEMM_L2PF: return v >= 0 && v <= 64;
     case CORTEX_KNOB_SK_KS: return v == -1 || (v >= 2 && v <= 4);

@@ -70,8 +70,15 @@ def weight_map(w: torch.Tensor) -> TensorMap:
     return TensorMap(w, 128)
 
 
+_ACT_BOX = None
+
+
 def act_map(x: torch.Tensor) -> TensorMap:
-    return TensorMap(x, 16)
+    """Activation (token) operand of the GEMMs: boxes of the rows the build expects."""
+    global _ACT_BOX
+    if _ACT_BOX is None:
+        _ACT_BOX = int(lib().cortex_act_box_rows())
+    return TensorMap(x, _ACT_BOX)
 
 
 def kv_map(cache2d: torch.Tensor) -> TensorMap:

@@ -79,13 +79,12 @@ def test_gemm_residual_and_f32(cuda, M):
 
 
 def _set_gemm_mode(o, mode):
-    """0 automatic, 1 = 1-SM kernel, 2 = 2-SM whole tiles, 3 = 2-SM stream-K, 4 = 2-SM
-    hybrid (whole tiles for the full waves, stream-K for the remainder, where it applies)."""
+    """0 automatic, 1 = 1-SM kernel, 2 = 2-SM whole tiles, 3 = 2-SM stream-K."""
     o.gemm_set_mode(min(mode, 2))
-    o.gemm_set_stream_k({0: -1, 1: -1, 2: 0, 3: 1, 4: 2}[mode])
+    o.gemm_set_stream_k({0: -1, 1: -1, 2: 0, 3: 1}[mode])
 
 
-@pytest.mark.parametrize("mode", [1, 2, 3, 4])
+@pytest.mark.parametrize("mode", [1, 2, 3])
 @pytest.mark.parametrize("M,N,K", [(129, 512, 256), (700, 4096, 4096), (300, 6144, 4096),
                                    (2048, 1536, 256), (33, 1024, 768), (1000, 28672, 4096),
                                    (4096, 4096, 14336), (5, 256, 4096)])
@@ -114,7 +113,7 @@ def test_gemm_paths_match(cuda, mode, M, N, K):
     assert rel(out32, ref + r) < 4e-5  # fp32 accumulation order over K <= 14336
 
 
-@pytest.mark.parametrize("mode", [1, 2, 3, 4])
+@pytest.mark.parametrize("mode", [1, 2, 3])
 @pytest.mark.parametrize("M,F,K", [(7, 768, 256), (300, 768, 256), (700, 14336, 4096),
                                    (64, 14336, 4096)])
 def test_gemm_fused_swiglu(cuda, mode, M, F, K):
