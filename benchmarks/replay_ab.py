@@ -9,8 +9,7 @@ kernels' alone (the KV values replayed are stale, the work is the same).
     python benchmarks/replay_ab.py [--record 60] [--rounds 3] [--variants base,plo0,...]
 Variants: base | plo0 (P as bf16 only) | norope (unfused RoPE / KV append) |
           logits (full lm_head logits + argmax) | pdl0 (no programmatic dependent launch) |
-          fmha1q / fmha2q (tcgen05 attention with one / two Q tiles per CTA, forced) |
-          nofuse (separate combine kernel, cascade on a side stream)
+          fmha1q / fmha2q (tcgen05 attention with one / two Q tiles per CTA, forced)
 """
 
 from __future__ import annotations
@@ -37,7 +36,6 @@ VARIANTS = {
     "logits": ({}, {"full_logits": True}),
     "pdl0": ({"PDL": 0}, {}),
     "fmha1q": ({"FMHA_2Q": 0}, {}),
-    "nofuse": ({}, {"fuse_decode_combine": False}),
     "fmha2q": ({"FMHA_2Q": 1}, {}),
 }
 

@@ -224,9 +224,7 @@ int32_t cortex_f32_attention(const float* q, const float* cache, int64_t k_row0,
  * selects the tcgen05 cascade pass.
  * parts (bitmask): 1 = shared-prefix cascade pass, 2 = per-call context splits, 4 = LSE
  * combine (7 = all), so the cascade pass can run on a second stream concurrently with
- * the splits (join before the combine); 8 = the combine folded into the splits (every
- * call's private context one split, max_splits = prefix_slots + 1, prefix_slots <= 8, the
- * cascade pass enqueued earlier on the same stream; e.g. parts 1 then 2 | 8). 
+ * the splits (join before the combine).
  * Balanced ("flat") plan (seq_tile_start != NULL): call b's tiles (its private tiles
  * under cascade, all tiles otherwise) are flat tiles [seq_tile_start[b],
  * seq_tile_start[b] + n_b) of one sequence of total_tiles; CTA (c, kv head) streams

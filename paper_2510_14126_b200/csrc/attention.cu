@@ -264,11 +264,6 @@ struct DecodeArgs {
   int max_splits;   // slots per sequence
   int cascade;      // 1: prefix tiles are handled by the shared-prefix kernel
   int slot_off;     // first slot of the private splits (cascade only)
-  // 1: every call's private context is ONE split and the cascade partials are complete
-  // (the cascade pass ran before on the same stream): the split merges them with its own
-  // state and writes the bf16 output directly (no o_part slot, no combine kernel)
-  int fuse_combine;
-  __nv_bfloat16* out;  // [B, Hq, 128] (fuse_combine)
 };
 
 constexpr int kDecodeStages = CORTEX_DECODE_STAGES;
@@ -432,19 +427,10 @@ CORTEX_DEVICE void dec_state_store(DecState& st, int warp, int group, float* cm,
 }
 
 // After a barrier: merge the 4 warps' states of query heads [0, group) and write the
-// partial (normalised O, LSE) of slot `slot` of call b — or, fused (a.fuse_combine), merge
-// it with the call's cascade prefix partials (slots [0, np)) in the combine kernel's order
-// and write the bf16 attention output.
+// partial (normalised O, LSE) of slot `slot` of call b.
 CORTEX_DEVICE void dec_merge_emit(const float* cm, const float* cl, const float* co, int co_rows,
                                   const DecodeArgs& a, int b, int kvh, int slot) {
   const int hq = a.n_kv_heads * a.group;
-  int np = 0;
-  if (a.fuse_combine && a.cascade) {
-    const int prefix = __ldg(&a.seq_prefix[b]);
-    const int npb = (prefix + kTile - 1) / kTile;
-    const int psb = npb ? prefix_split_blocks(npb, a.slot_off) : 1;
-    np = (npb + psb - 1) / psb;
-  }
   for (int idx = threadIdx.x; idx < a.group * kHeadDim; idx += blockDim.x) {
     const int r = idx / kHeadDim;
     const int d = idx % kHeadDim;
@@ -460,29 +446,6 @@ CORTEX_DEVICE void dec_merge_emit(const float* cm, const float* cl, const float*
       O += co[(w * co_rows + r) * kHeadDim + d] * f;
     }
     const int h = kvh * a.group + r;
-    if (a.fuse_combine) {
-      // the combine's weighted sum over [cascade slots..., this split]
-      const float o_own = O / L, lse_own = M + log2f(L);
-      const int64_t base = static_cast<int64_t>(b) * a.max_splits;
-      float lse[8], ov[8];
-      float Mx = lse_own;
-      for (int i = 0; i < np; ++i) {
-        lse[i] = a.lse_part[(base + i) * hq + h];
-        ov[i] = a.o_part[((base + i) * hq + h) * kHeadDim + d];
-        Mx = fmaxf(Mx, lse[i]);
-      }
-      float Lt = 0.f, acc = 0.f;
-      for (int i = 0; i < np; ++i) {
-        const float w = exp2f(lse[i] - Mx);
-        Lt += w;
-        acc += w * ov[i];
-      }
-      const float w = exp2f(lse_own - Mx);
-      Lt += w;
-      acc += w * o_own;
-      a.out[(static_cast<int64_t>(b) * hq + h) * kHeadDim + d] = __float2bfloat16_rn(acc / Lt);
-      continue;
-    }
     const int64_t pidx = (static_cast<int64_t>(b) * a.max_splits + slot) * hq + h;
     a.o_part[pidx * kHeadDim + d] = O / L;
     if (d == 0) a.lse_part[pidx] = M + log2f(L);
@@ -1220,13 +1183,6 @@ int32_t cortex_paged_decode_attn(
   a.max_splits = max_splits;
   a.cascade = cascade;
   a.slot_off = cascade ? prefix_slots : 0;
-  // parts & 8: the combine folded into the context splits (the caller guarantees one
-  // private split per call, <= 8 prefix slots, and the cascade pass already enqueued
-  // before on this stream; not with the flat plan)
-  a.fuse_combine = (parts & 8) && !seq_tile_start ? 1 : 0;
-  a.out = reinterpret_cast<__nv_bfloat16*>(out);
-  if (a.fuse_combine && (max_splits - a.slot_off != 1 || (cascade && prefix_slots > 8)))
-    return CORTEX_EBADARG;
   const int smem = kWarps * kDecodeStages * kStageBytes + 1024 + 256;
   static bool configured = false;
   if (!configured) {
@@ -1261,7 +1217,7 @@ int32_t cortex_paged_decode_attn(
                    *reinterpret_cast<const CUtensorMap*>(tmap_kv), a) != cudaSuccess)
       return CORTEX_ECUDA;
   }
-  if (!(parts & 4) || a.fuse_combine) return CORTEX_OK;
+  if (!(parts & 4)) return CORTEX_OK;
   CombineArgs cb{};
   cb.o_part = o_part;
   cb.lse_part = lse_part;

@@ -283,9 +283,6 @@ class GpuWorker:
         self.tc_attention = os.environ.get("CORTEX_TC_ATTN", "1") != "0"
         self.qmap = ops.QMap(self.q, cfg.n_heads, cfg.group)
         self.overlap_cascade = True
-        # the LSE combine folded into the decode context splits when every call has one
-        # private split (the cascade pass then runs before them on the main stream)
-        self.fuse_decode_combine = True
         # prefix slots of the cascade pass: 0 = by prefix length (below), or a fixed count
         self.cascade_slots = int(os.environ.get("CORTEX_CASCADE_SLOTS", "0"))
         # balanced decode plan (equal tile ranges per CTA) instead of per-call 512-token
@@ -659,33 +656,7 @@ class GpuWorker:
                 dargs = (self.kvmap, self.q, self.table, d_drow, d_dpre, d_dkv, n_dec, hkv,
                          cfg.group, k0, v0, self.scale, o_part, lse_part, max_splits, self.attn)
                 qmap = self.qmap if self.tc_attention else None
-
-                def ctx_splits(parts=2):
-                    e2 = prof.open("attn_decode_ctx") if prof is not None else None
-                    ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=parts,
-                                          flat=flat)
-                    if e2 is not None:
-                        prof.close("attn_decode_ctx", e2, ctx_bytes, ctx_flops)
-
-                if (dec_groups is not None and qmap is not None and self.fuse_decode_combine
-                        and fplan is None and max_splits == pslots + 1 and pslots <= 8):
-                    # every call's private context is one split: the cascade pass, then the
-                    # splits with the LSE combine folded in, on the main stream; the prompt
-                    # prefill (tensor) on a side stream concurrently
-                    main = torch.cuda.current_stream()
-                    if n_pf:
-                        self._ev_fork.record(main)
-                        self.side.wait_event(self._ev_fork)
-                        prefill_attn(self.side)
-                        pf_done = True
-                        nl += 1
-                    ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=1)
-                    ctx_splits(parts=2 | 8)
-                    if n_pf:
-                        self._ev_join.record(self.side)
-                        main.wait_event(self._ev_join)
-                    nl -= 1  # (no combine launch)
-                elif dec_groups is not None and qmap is not None and self.overlap_cascade:
+                if dec_groups is not None and qmap is not None and self.overlap_cascade:
                     # tensor-core passes - the shared-prefix (cascade) pass, then the prompt
                     # prefill - on a side stream, concurrent with the per-call context splits
                     # (HBM) on the main stream; join before the LSE combine. (The decode
@@ -693,6 +664,14 @@ class GpuWorker:
                     main = torch.cuda.current_stream()
                     self._ev_fork.record(main)
                     self.side.wait_event(self._ev_fork)
+
+                    def ctx_splits():
+                        e2 = prof.open("attn_decode_ctx") if prof is not None else None
+                        ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=2,
+                                              flat=flat)
+                        if e2 is not None:
+                            prof.close("attn_decode_ctx", e2, ctx_bytes, ctx_flops)
+
                     ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=1,
                                           stream=self.side)
                     if n_pf:

@@ -339,11 +339,9 @@ def test_paged_decode_attention(cuda, group, flat):
 
 @pytest.mark.parametrize("group", [4, 2])
 @pytest.mark.parametrize("plens", [(1000, 40), (8192,), (16, 5, 0)])
-@pytest.mark.parametrize("impl", ["mma", "tc", "tc1", "tc-flat", "tc-fused"])
+@pytest.mark.parametrize("impl", ["mma", "tc", "tc1", "tc-flat"])
 def test_cascade_decode_attention(cuda, group, plens, impl):
-    """Shared-prefix decode: calls grouped by resident prefix, prefix attended once.
-    tc-fused: one private split per call, the cascade pass first, then the splits with the
-    LSE combine folded in (parts 1, then 2 | 8)."""
+    """Shared-prefix decode: calls grouped by resident prefix, prefix attended once."""
     o = ops()
     hkv, nb = 2, 2048
     hq = hkv * group
@@ -368,8 +366,6 @@ def test_cascade_decode_attention(cuda, group, plens, impl):
         for i in range(counts[g]):
             # ragged private lengths, some past one 512-token split (a 1-3 tile 2nd split)
             priv = int(rng.integers(1, 300)) if i % 3 else int(rng.integers(513, 560))
-            if impl == "tc-fused":
-                priv = min(priv, 512)  # one private split
             npr = (priv + 15) // 16
             ids = pref_blocks[g] + [perm.pop() for _ in range(npr)]
             table[r, :len(ids)] = torch.tensor(ids, dtype=torch.int32)
@@ -402,15 +398,10 @@ def test_cascade_decode_attention(cuda, group, plens, impl):
     o.fmha_set_2q(0 if impl == "tc1" else 1)
     plo = _lib.set_knob("FMHA_PLO", 0 if impl == "tc-bf16p" else 1)
     try:
-        args = (o.kv_map(cache.view(-1, 128)), q, table, dev(seq_row), dev(seq_pre), dev(seq_kv),
-                B, hkv, group, k0, v0, 1 / math.sqrt(128), o_part, lse_part, max_splits, out)
-        qmap = o.QMap(q, hq, group) if impl != "mma" else None
-        if impl == "tc-fused":
-            assert max_splits == pslots + 1
-            o.paged_decode_attn(*args, groups=groups, qmap=qmap, parts=1)
-            o.paged_decode_attn(*args, groups=groups, qmap=qmap, parts=2 | 8)
-        else:
-            o.paged_decode_attn(*args, groups=groups, qmap=qmap, flat=plan)
+        o.paged_decode_attn(o.kv_map(cache.view(-1, 128)), q, table, dev(seq_row), dev(seq_pre),
+                            dev(seq_kv), B, hkv, group, k0, v0, 1 / math.sqrt(128), o_part,
+                            lse_part, max_splits, out, groups=groups,
+                            qmap=o.QMap(q, hq, group) if impl != "mma" else None, flat=plan)
     finally:
         o.fmha_set_2q(-1)
         _lib.set_knob("FMHA_PLO", plo)
