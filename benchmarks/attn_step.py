@@ -36,6 +36,7 @@ def build(n_calls=215, n_pf=3, pf_len=200, slots=2, seed=0, layers=4):
     dev = torch.device("cuda")
     npb = (P + 15) // 16
     priv = rng.integers(110, 451, n_calls)
+    priv = (priv * float(os.environ.get("CORTEX_PRIV_SCALE", "1"))).astype(np.int64)
     nbs = [(int(p) + 15) // 16 for p in priv]
     pf_nb = (pf_len + 15) // 16
     nb = 2 * npb + sum(nbs) + n_pf * pf_nb + 64
@@ -84,6 +85,9 @@ def build(n_calls=215, n_pf=3, pf_len=200, slots=2, seed=0, layers=4):
     persplit = max(max(ops.decode_splits(0, int(p)) for p in priv),
                    max(ops.decode_splits(0, P + int(p)) for p in priv))
     st["max_splits"] = st["max_splits_cap"] = slots + max(persplit, plan[3], 8)
+    # the model's slot count (pslots + the most private splits of a call): sizes the
+    # per-call split grid of the context-split kernels
+    st["max_splits_tight"] = slots + max(ops.decode_splits(0, int(p)) for p in priv)
     st["o_part"] = torch.empty(n_calls * st["max_splits"] * HQ * 128, device=dev)
     st["lse"] = torch.empty(n_calls * st["max_splits"] * HQ, device=dev)
     st["kvmap"] = ops.kv_map(cache.view(-1, 128))
@@ -110,7 +114,9 @@ def decode(st, layer, parts, stream=None, flat="default"):
     groups = (st["grow"], st["gplen"], st["gfirst"], st["gcount"], 2, st["gmax"], st["pslots"])
     ops.paged_decode_attn(st["kvmap"], st["q"], st["table"], st["drow"], st["dpre"], st["dkv"],
                           st["n_calls"], HKV, GROUP, 2 * layer * pl, (2 * layer + 1) * pl,
-                          1 / math.sqrt(128), st["o_part"], st["lse"], st["max_splits"],
+                          1 / math.sqrt(128), st["o_part"], st["lse"],
+                          st["max_splits_tight"] if (flat if flat != "default" else st["flat"]) is None
+                          else st["max_splits"],
                           st["attn"], groups=groups, qmap=st["qmap"], parts=parts, stream=stream,
                           flat=st["flat"] if flat == "default" else flat)
 
@@ -194,7 +200,20 @@ def timed(st, fn, iters=40):
 
 
 def main():
+    from paper_2510_14126_b200 import _lib
+
+    for kv in filter(None, os.environ.get("CORTEX_KNOBS", "").split(",")):  # NAME=V,...
+        k, v = kv.split("=")
+        _lib.set_knob(k, int(v))
     st = build(slots=int(os.environ.get("CORTEX_CASCADE_SLOTS", "2")))
+    if "--private-only" in sys.argv:  # tuning-variant sweeps: the context splits alone
+        us = timed(st, lambda l: decode(st, l, 2, flat=None))
+        gbs = st["priv_tokens"] * HKV * 128 * 2 * 2 / us / 1e3
+        print(json.dumps({"private_us": us, "private_GBps": gbs,
+                          "lib": os.environ.get("CORTEX_LIB", ""),
+                          "knobs": os.environ.get("CORTEX_KNOBS", ""),
+                          "priv_scale": os.environ.get("CORTEX_PRIV_SCALE", "1")}), flush=True)
+        return
     if "--once" in sys.argv:  # for ncu: 2 x (private, cascade, combine, prefill)
         for i in range(2):
             decode(st, i, 2)

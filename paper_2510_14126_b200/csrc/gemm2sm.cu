@@ -275,8 +275,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           const uint32_t full_leader = mapa_shared(smem_u32(&full[s]), 0);
+#if defined(CORTEX_G2_NOFEED)  // tuning builds only: MMA issue rate without operand traffic
+          if (it >= STAGES) {
+            if (leader)
+              mbar_arrive(&full[s]);
+            else
+              mbar_arrive_cluster(full_leader);
+            continue;
+          }
+#endif
+#if defined(CORTEX_G2_NOFEED) || defined(CORTEX_G2_NOFEED_X)
+          constexpr uint32_t kExpect = 2 * L::kA;  // the weights only
+#else
+          constexpr uint32_t kExpect = 2 * L::kStage;
+#endif
           if (leader)
-            mbar_arrive_expect_tx(&full[s], 2 * L::kStage);
+            mbar_arrive_expect_tx(&full[s], kExpect);
           else
             mbar_arrive_cluster(full_leader);
           tma_load_2d_2sm(smem + s * L::kStage, &tmap_w, full_leader, kb * kBK, n0);
@@ -291,10 +305,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
       // (benchmarks/micro/tma_tile.cu: 235 MB of weights in 47 us with one issuer,
       // 40 us with two). The stage's expected bytes were armed by warp 0 (or are
       // counted before the arm: the transaction count may go transiently negative).
+#if defined(CORTEX_G2_NOFEED) || defined(CORTEX_G2_NOFEED_X)
+      constexpr bool kFeedX = false;
+#else
+      constexpr bool kFeedX = true;
+#endif
       uint32_t it = 0;
       int pos = seg_start(args, pair);
       Seg g;
-      while (seg_next(args, pair, pos, g)) {
+      while (kFeedX && seg_next(args, pair, pos, g)) {
         const int m_tile = g.t % args.m_tiles;
         const int x0 = m_tile * TN + rank * (TN / 2);
         for (int kb = g.kb0; kb < g.kb1; ++kb, ++it) {

@@ -111,10 +111,14 @@ class KernelProfile:
 
     Each record: (class, start event, end event, algorithmic bytes, flops)."""
 
-    def __init__(self, classes, every: int = 1) -> None:
+    def __init__(self, classes, every: int = 1, isolate: bool = False) -> None:
         self.classes = set(classes)
         self.recs: list = []
         self.every = every  # time the kernels of one step in `every` (event overhead)
+        # isolate: the sampled steps run their attention passes one after another on the
+        # main stream (no side-stream overlap), so each class's events bracket that class
+        # alone - per-class rooflines, not the schedule's overlap
+        self.isolate = isolate
 
     def sampled(self, step: int) -> bool:
         return step % self.every == 0
@@ -656,7 +660,19 @@ class GpuWorker:
                 dargs = (self.kvmap, self.q, self.table, d_drow, d_dpre, d_dkv, n_dec, hkv,
                          cfg.group, k0, v0, self.scale, o_part, lse_part, max_splits, self.attn)
                 qmap = self.qmap if self.tc_attention else None
-                if dec_groups is not None and qmap is not None and self.overlap_cascade:
+                isolate = prof is not None and prof.isolate
+                if dec_groups is not None and qmap is not None and isolate:
+                    # profiled in isolation: cascade pass, context splits (timed alone),
+                    # combine; the prompt prefill follows as its own class
+                    ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=1)
+                    e2 = prof.open("attn_decode_ctx")
+                    ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=2,
+                                          flat=flat)
+                    if e2 is not None:
+                        prof.close("attn_decode_ctx", e2, ctx_bytes, ctx_flops)
+                    ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=4,
+                                          flat=flat)
+                elif dec_groups is not None and qmap is not None and self.overlap_cascade:
                     # tensor-core passes - the shared-prefix (cascade) pass, then the prompt
                     # prefill - on a side stream, concurrent with the per-call context splits
                     # (HBM) on the main stream; join before the LSE combine. (The decode
