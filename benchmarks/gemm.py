@@ -58,6 +58,11 @@ def bench(M: int, name: str, iters: int = 20, residual: bool = False) -> dict:
 if __name__ == "__main__":
     if os.environ.get("GEMM_MODE"):  # 1: 1-SM, 2: 2-SM whole tiles, 3: cluster split-K
         ops.gemm_set_mode(int(os.environ["GEMM_MODE"]))
+    from paper_2510_14126_b200 import _lib
+
+    for kv in filter(None, os.environ.get("CORTEX_KNOBS", "").split(",")):  # NAME=V,...
+        k, v = kv.split("=")
+        _lib.set_knob(k, int(v))
     Ms = [int(a) for a in sys.argv[1:]] or [32, 128, 256, 700, 2048, 4096]
     for M in Ms:
         for name in SHAPES:

@@ -1,10 +1,11 @@
 """Is a config-2 step GPU-bound or host-bound?
 
 Runs the bench runtime and splits the host wall time of each step into: time the
-host spent blocked on the GPU (waiting for a staging-ring slot, i.e. the GPU is
-behind), time inside GpuWorker.forward (Python + launches), and scheduler time
-(dispatch, planning, completions). If "blocked" is a large share, the GPU is the
-bottleneck; if it is near zero the host is.
+host spent blocked on a staging-ring slot, time inside GpuWorker.forward (Python +
+launches; a launch also waits here when the GPU's launch queue is full, so with the GPU
+behind, forward's time is the GPU's pace, not host work), and scheduler time (dispatch,
+planning, completions). Then forward's host cost alone: 40 steps each started on a
+drained GPU, with the layer loop in Python and in native code (csrc/step.cu).
 """
 
 from __future__ import annotations
@@ -72,6 +73,20 @@ def main(steps: int = 300) -> None:
            "blocked_ms_per_step": 1e3 * acc["blocked"] / steps,
            "forward_ms_per_step (incl. blocked)": 1e3 * acc["forward"] / steps,
            "scheduler_ms_per_step": 1e3 * (wall - acc["forward"]) / steps}
+    # host submission cost alone: the GPU drained before every step, so no launch can
+    # wait for queue space; forward's wall time is then pure host work (per the layer loop
+    # in Python vs native csrc/step.cu)
+    sub = {}
+    for native in (True, False):
+        w.native_layers = native
+        acc["forward"] = 0.0
+        for _ in range(40):
+            torch.cuda.synchronize()
+            rt.step()
+        torch.cuda.synchronize()
+        sub["native" if native else "python"] = 1e3 * acc["forward"] / 40
+    w.native_layers = True
+    out["host_forward_ms_gpu_idle"] = sub
     print(json.dumps(out), flush=True)
 
 

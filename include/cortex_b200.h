@@ -271,6 +271,67 @@ int32_t cortex_fmha_cascade_tc(const void* tmap_kv, const void* tmap_q, const in
                                float* o_part, float* lse_part, int32_t max_splits,
                                cortex_stream_t stream);
 
+/* ---- a decoder step's layer loop from native code -----------------------------------
+ * The layers [layer_begin, layer_end) of one step (the GPU work behind an engine step's
+ * admit prefills and advance_decode tokens, stagesim/engines.py:142-194), launched in the
+ * order and with the arguments the per-op exports above take one call at a time: per
+ * layer cortex_rmsnorm (attn_norm) -> cortex_gemm_qkv_rope -> decode attention
+ * (cortex_paged_decode_attn; with cascade groups and a side stream: parts 1 + the
+ * prompt prefill on side_stream, parts 2 on stream, join, parts 4) -> prompt prefill
+ * (cortex_fmha_prefill_tc, when not on the side stream) -> O projection + residual
+ * (mode 1) -> cortex_rmsnorm (mlp_norm) -> gate/up with SwiGLU (mode 2) -> down +
+ * residual (mode 1). cortex_decoder_t describes the model (built once); cortex_step_t
+ * one step (device metadata uploaded by the caller; embed, rope_token_prep, final norm
+ * and lm_head stay with the caller). Weight tensor maps are the 128-byte host
+ * CUtensorMaps of cortex_tmap_encode_2d_bf16 (wgu rows interleaved as mode 2 expects);
+ * tmap_xn / tmap_attn / tmap_act are the activation maps (box rows cortex's GEMMs
+ * use), tmap_q from cortex_tmap_encode_q (required: the tcgen05 attention). K / V of
+ * layer l are the 128-wide cache rows starting at 2 l plane_rows / (2 l + 1) plane_rows.
+ * Returns the first failing launch's status. */
+typedef struct {
+  int32_t n_layers, d_model, hq, hkv, ffn;
+  float eps, softmax_scale;
+  const void* const* tmap_wqkv; /* [n_layers] */
+  const void* const* tmap_wo;
+  const void* const* tmap_wgu;
+  const void* const* tmap_wd;
+  const void* const* attn_norm; /* [n_layers] device bf16 [d_model] */
+  const void* const* mlp_norm;
+  const void* tmap_xn;
+  const void* tmap_attn;
+  const void* tmap_act;
+  const void* tmap_kv;
+  const void* tmap_q;
+  float* x;    /* fp32 residual stream [>= n_tok, d_model] */
+  void* xn;    /* bf16 [>= n_tok, d_model] */
+  void* q;     /* bf16 [>= n_tok, hq * 128] */
+  void* attn;  /* bf16 [>= n_tok, hq * 128] */
+  void* act;   /* bf16 [>= n_tok, ffn] */
+  void* cache;
+  int64_t plane_rows;
+  const int32_t* table;
+  int32_t table_stride;
+  const int32_t* tok_dst; /* cortex_rope_token_prep outputs of the step */
+  const float* tok_cs;
+  float* workspace;
+  uint64_t workspace_bytes;
+  int32_t* counters;
+  int32_t n_counters;
+} cortex_decoder_t;
+typedef struct {
+  int32_t n_tok, n_dec, n_pf, max_qlen, max_splits;
+  int32_t layer_begin, layer_end;
+  const int32_t *dec_row, *dec_prefix, *dec_kvlen;                      /* [n_dec] */
+  const int32_t *pf_row, *pf_prefix, *pf_kvlen, *pf_qstart, *pf_qlen;   /* [n_pf] */
+  const int32_t *grp_row, *grp_plen, *grp_first, *grp_count;            /* [n_groups] */
+  int32_t n_groups, max_group_count, prefix_slots;
+  float* o_part;
+  float* lse_part;
+  cortex_stream_t stream;
+  cortex_stream_t side_stream; /* NULL: every attention pass on stream */
+} cortex_step_t;
+int32_t cortex_decoder_layers(const cortex_decoder_t* model, const cortex_step_t* step);
+
 /* ---- Tensor parallelism (TP = 2 inside one engine replica, BASELINE config 5) -------
  * the only collective on the path. The reference engine has no
  * model and hence no TP (engines.py:101-246); these exports implement the

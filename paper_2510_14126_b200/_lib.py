@@ -51,6 +51,7 @@ SIGNATURES: dict[str, list] = {
                                P],
     "cortex_fmha_cascade_tc": [P, P, P, I32, P, P, P, P, I32, I32, I32, I32, I32, I64, I64, F32,
                                P, P, I32, P],
+    "cortex_decoder_layers": [P, P],
     "cortex_sym_alloc": [U64, P],
     "cortex_sym_free": [P],
     "cortex_ipc_get_handle": [P, P],
@@ -85,6 +86,34 @@ class RopeEpilogue(ctypes.Structure):
 
     _fields_ = [("q_out", P), ("cache", P), ("k_row0", I64), ("v_row0", I64), ("tok_dst", P),
                 ("tok_cs", P), ("hq", I32), ("hkv", I32)]
+
+
+class DecoderDesc(ctypes.Structure):
+    """cortex_decoder_t (include/cortex_b200.h)."""
+
+    _fields_ = [("n_layers", I32), ("d_model", I32), ("hq", I32), ("hkv", I32), ("ffn", I32),
+                ("eps", F32), ("softmax_scale", F32),
+                ("tmap_wqkv", P), ("tmap_wo", P), ("tmap_wgu", P), ("tmap_wd", P),
+                ("attn_norm", P), ("mlp_norm", P),
+                ("tmap_xn", P), ("tmap_attn", P), ("tmap_act", P), ("tmap_kv", P),
+                ("tmap_q", P),
+                ("x", P), ("xn", P), ("q", P), ("attn", P), ("act", P), ("cache", P),
+                ("plane_rows", I64), ("table", P), ("table_stride", I32),
+                ("tok_dst", P), ("tok_cs", P),
+                ("workspace", P), ("workspace_bytes", U64), ("counters", P), ("n_counters", I32)]
+
+
+class StepDesc(ctypes.Structure):
+    """cortex_step_t (include/cortex_b200.h)."""
+
+    _fields_ = [("n_tok", I32), ("n_dec", I32), ("n_pf", I32), ("max_qlen", I32),
+                ("max_splits", I32), ("layer_begin", I32), ("layer_end", I32),
+                ("dec_row", P), ("dec_prefix", P), ("dec_kvlen", P),
+                ("pf_row", P), ("pf_prefix", P), ("pf_kvlen", P), ("pf_qstart", P),
+                ("pf_qlen", P),
+                ("grp_row", P), ("grp_plen", P), ("grp_first", P), ("grp_count", P),
+                ("n_groups", I32), ("max_group_count", I32), ("prefix_slots", I32),
+                ("o_part", P), ("lse_part", P), ("stream", P), ("side_stream", P)]
 
 
 STATUS_NAMES = {0: "ok", -1: "bad argument", -2: "CUDA error", -3: "out of KV blocks",

@@ -12,6 +12,7 @@ stream per step, every projection a tcgen05 GEMM.
 
 from __future__ import annotations
 
+import ctypes
 import math
 import os
 from dataclasses import dataclass, field
@@ -19,7 +20,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import ops
+from . import _lib, ops
 from .config import BLOCK_TOKENS, HEAD_DIM, ModelConfig
 
 BF16 = torch.bfloat16
@@ -295,6 +296,12 @@ class GpuWorker:
         self.side = torch.cuda.Stream(device=dev)
         self._ev_fork = torch.cuda.Event()
         self._ev_join = torch.cuda.Event()
+        # layer loop launched from native code (csrc/step.cu, one ctypes call per step)
+        # instead of ~10 ctypes calls per layer; the Python loop stays for TP, the
+        # per-class profile window and the non-default A/B paths
+        self.native_layers = True
+        self._native = None
+        self._step_desc = _lib.StepDesc()
 
     def _init_f32(self, cfg, device, n_blocks, n_rows, row_cols, max_tokens, max_out, hist_cols,
                   max_seq_tokens, weights, seed) -> None:
@@ -351,6 +358,35 @@ class GpuWorker:
             k = f"layers.{i}.wgu"
             out[k] = ops.deinterleave_gate_up(self.w[k])
         return out
+
+    def _native_desc(self):
+        """cortex_decoder_t of this worker (built once; keeps its pointer arrays alive)."""
+        if self._native is None:
+            cfg, wm, w = self.cfg, self.wmap, self.w
+            L = cfg.n_layers
+            arr = lambda vals: (ctypes.c_void_p * L)(*vals)
+            keep = {
+                "wqkv": arr([wm[f"layers.{i}.wqkv"].ptr for i in range(L)]),
+                "wo": arr([wm[f"layers.{i}.wo"].ptr for i in range(L)]),
+                "wgu": arr([wm[f"layers.{i}.wgu"].ptr for i in range(L)]),
+                "wd": arr([wm[f"layers.{i}.wd"].ptr for i in range(L)]),
+                "n1": arr([w[f"layers.{i}.attn_norm"].data_ptr() for i in range(L)]),
+                "n2": arr([w[f"layers.{i}.mlp_norm"].data_ptr() for i in range(L)]),
+            }
+            ws = self.gemm_ws
+            d = _lib.DecoderDesc(
+                L, cfg.d_model, cfg.n_heads, cfg.n_kv_heads, cfg.ffn, cfg.eps, self.scale,
+                ctypes.cast(keep["wqkv"], ctypes.c_void_p), ctypes.cast(keep["wo"], ctypes.c_void_p),
+                ctypes.cast(keep["wgu"], ctypes.c_void_p), ctypes.cast(keep["wd"], ctypes.c_void_p),
+                ctypes.cast(keep["n1"], ctypes.c_void_p), ctypes.cast(keep["n2"], ctypes.c_void_p),
+                self.xn_map.ptr, self.attn_map.ptr, self.act_map.ptr, self.kvmap.ptr,
+                self.qmap.ptr, self.x.data_ptr(), self.xn.data_ptr(), self.q.data_ptr(),
+                self.attn.data_ptr(), self.act.data_ptr(), self.cache.data_ptr(),
+                self.layer_rows(1)[0] // 2, self.table.data_ptr(), self.table.stride(0),
+                self.tok_dst.data_ptr(), self.tok_cs.data_ptr(), ws.ws.data_ptr(),
+                ws.ws.numel() * 4, ws.counters.data_ptr(), ws.counters.numel())
+            self._native = (d, keep)
+        return self._native[0]
 
     def layer_rows(self, layer: int) -> tuple[int, int]:
         per_plane = self.n_blocks * self.cfg.n_kv_heads * BLOCK_TOKENS
@@ -622,7 +658,33 @@ class GpuWorker:
             ops.rope_token_prep(self.table, d_pos, d_arow, d_acol, d_aoff, self.cos, self.sin, T,
                                 hkv, self.tok_dst, self.tok_cs)
             nl += 1
-        for li in range(cfg.n_layers):
+        native = (self.native_layers and tp is None and prof is None and self.fuse_qkv_rope
+                  and self.tc_attention and flat is None)
+        if native:
+            sd = self._step_desc
+            ptr = lambda t: t.data_ptr() if t is not None and t.numel() else None
+            sd.n_tok, sd.n_dec, sd.n_pf, sd.max_qlen, sd.max_splits = (T, n_dec, n_pf, max_qlen,
+                                                                       max_splits)
+            sd.layer_begin, sd.layer_end = 0, cfg.n_layers
+            sd.dec_row, sd.dec_prefix, sd.dec_kvlen = ptr(d_drow), ptr(d_dpre), ptr(d_dkv)
+            sd.pf_row, sd.pf_prefix, sd.pf_kvlen = ptr(d_prow), ptr(d_ppre), ptr(d_pkv)
+            sd.pf_qstart, sd.pf_qlen = ptr(d_pqs), ptr(d_pql)
+            if dec_groups is not None:
+                sd.grp_row, sd.grp_plen, sd.grp_first, sd.grp_count = (
+                    ptr(t) for t in dec_groups[:4])
+                sd.n_groups, sd.max_group_count, sd.prefix_slots = dec_groups[4:]
+            else:
+                sd.grp_row = sd.grp_plen = sd.grp_first = sd.grp_count = None
+                sd.n_groups = sd.max_group_count = sd.prefix_slots = 0
+            sd.o_part, sd.lse_part = o_part.data_ptr(), lse_part.data_ptr()
+            sd.stream = torch.cuda.current_stream().cuda_stream
+            sd.side_stream = self.side.cuda_stream if self.overlap_cascade else None
+            ops._check(ops.lib().cortex_decoder_layers(ctypes.byref(self._native_desc()),
+                                                       ctypes.byref(sd)),
+                       "cortex_decoder_layers")
+            # launches, counted as the Python loop counts them
+            nl += cfg.n_layers * (6 + (2 if n_dec else 0) + (1 if n_pf else 0))
+        for li in range(0 if not native else cfg.n_layers, cfg.n_layers):
             p = f"layers.{li}."
             k0, v0 = self.layer_rows(li)
             if tp is None or li == 0:  # TP: fused into the previous layer's down exchange
