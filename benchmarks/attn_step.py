@@ -214,6 +214,12 @@ def main():
                           "knobs": os.environ.get("CORTEX_KNOBS", ""),
                           "priv_scale": os.environ.get("CORTEX_PRIV_SCALE", "1")}), flush=True)
         return
+    if "--fmha-only" in sys.argv:  # tuning-variant sweeps: the tensor-core passes alone
+        print(json.dumps({"prefill_us": timed(st, lambda l: prefill(st, l)),
+                          "cascade_us": timed(st, lambda l: decode(st, l, 1)),
+                          "lib": os.environ.get("CORTEX_LIB", ""),
+                          "knobs": os.environ.get("CORTEX_KNOBS", "")}), flush=True)
+        return
     if "--once" in sys.argv:  # for ncu: 2 x (private, cascade, combine, prefill)
         for i in range(2):
             decode(st, i, 2)

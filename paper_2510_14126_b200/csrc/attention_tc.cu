@@ -391,8 +391,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint32_t off = (kk >> 2) * kKVHalf + (kk & 3) * 32;
+#ifndef CORTEX_FMHA_NOMMA
             umma_bf16_ss(tmem_s + 128 * s, umma_desc_sw128(q_addr + off),
                          umma_desc_sw128(k_addr + off), idesc_s, kk != 0 ? 1u : 0u);
+#endif
           }
           umma_commit(&k_empty[s]);
           umma_commit(&s_full[s]);
@@ -411,9 +413,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           for (int part = 0; part < 1 + a.p_lo; ++part) {
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
+#ifndef CORTEX_FMHA_NOMMA
               umma_bf16_ts(tmem_o, p_tmem + 64 * part + 8 * kk,
                            umma_desc_sw128_mn(v_addr + kk * 2048, kKVHalf), idesc_pv,
                            (t | kk | part) != 0 ? 1u : 0u);
+#endif
             }
           }
           umma_commit(&v_empty[s]);
@@ -442,6 +446,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       const int s = kt % kStagesTC;
       mbar_wait_guard(&s_full[s], (kt / kStagesTC) & 1);
       tc_fence_after();
+#ifdef CORTEX_FMHA_NOSOFTMAX
+      if (true) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full);
+        continue;
+      }
+#endif
       float sv[64];
       {
         uint32_t u0[32], u1[32];  // both loads in flight, one wait
@@ -749,8 +761,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t off = (kk >> 2) * kKVHalf + (kk & 3) * 32;
+#ifndef CORTEX_FMHA_NOMMA  // (tuning builds only: pipeline bound without the MMAs)
           umma_bf16_ss(tmem + 128 * x + 64 * h, umma_desc_sw128(q_addr + off),
                        umma_desc_sw128(k_addr + off), idesc_s, kk != 0 ? 1u : 0u);
+#endif
         }
         umma_commit(&s_full[2 * x + h]);
       };
@@ -763,9 +777,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         for (int part = 0; part < 1 + a.p_lo; ++part) {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
+#ifndef CORTEX_FMHA_NOMMA
             umma_bf16_ts(o_tmem, p_tmem + 32 * part + 8 * kk,
                          umma_desc_sw128_mn(v_addr + (4 * h + kk) * 2048, kKVHalf), idesc_pv,
                          (kt | h | kk | part) != 0 ? 1u : 0u);
+#endif
           }
         }
         umma_commit(&o_ready[x]);
@@ -820,6 +836,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const int kt = u >> 1, h = u & 1;
         mbar_wait_guard(&s_full[2 * x + h], kt & 1);
         tc_fence_after();
+#ifdef CORTEX_FMHA_NOSOFTMAX  // (tuning builds only: pipeline bound without the softmax)
+        if (true) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[2 * x + h]);
+          continue;
+        }
+#endif
         float sv[64];
         {
           uint32_t u0[32], u1[32];  // both loads in flight, one wait
