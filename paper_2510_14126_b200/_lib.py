@@ -66,6 +66,7 @@ SIGNATURES: dict[str, list] = {
 DEV_SIGNATURES: dict[str, list] = {
     "cortex_dev_set_knob": [I32, I32],
     "cortex_dev_get_knob": [I32],
+    "cortex_dev_last_cuda_error": [],
     "cortex_gemm_splits": [I32, I32, I32],
     "cortex_gemm_path": [I32, I32, I32],
     "cortex_gemm2_tile": [I32, I32, I32],

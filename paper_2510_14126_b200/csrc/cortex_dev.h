@@ -35,6 +35,8 @@ enum CortexKnob {
 
 int32_t cortex_dev_set_knob(int32_t knob, int32_t value);
 int32_t cortex_dev_get_knob(int32_t knob);
+/* cudaGetLastError() of the library's runtime (diagnosing a CORTEX_ECUDA status). */
+int32_t cortex_dev_last_cuda_error(void);
 
 /* Introspection of the GEMM planner (host functions). */
 int32_t cortex_gemm_splits(int32_t M, int32_t N, int32_t K);

@@ -254,6 +254,8 @@ int32_t cortex_dev_set_knob(int32_t knob, int32_t value) {
   return CORTEX_OK;
 }
 
+int32_t cortex_dev_last_cuda_error(void) { return static_cast<int32_t>(cudaGetLastError()); }
+
 int32_t cortex_dev_get_knob(int32_t knob) {
   if (knob < 0 || knob >= CORTEX_KNOB_COUNT) return CORTEX_EBADARG;
   return g_cortex_knob[knob];
