@@ -17,7 +17,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from paper_2510_14126_b200 import ops  # noqa: E402
 
-SHAPES = {"qkv": (6144, 4096), "o": (4096, 4096), "gate_up": (28672, 4096), "down": (4096, 14336)}
+SHAPES = {"qkv": (6144, 4096), "o": (4096, 4096), "gate_up": (28672, 4096), "down": (4096, 14336),
+          "lm_head": (128256, 4096)}
 
 
 def bench(M: int, name: str, iters: int = 20, residual: bool = False) -> dict:
@@ -28,16 +29,18 @@ def bench(M: int, name: str, iters: int = 20, residual: bool = False) -> dict:
     maps = [ops.weight_map(w) for w in ws]
     x = torch.randn(max(M, 32), K, device=dev).to(torch.bfloat16)
     xm = ops.act_map(x)
-    out = torch.empty(M, N, device=dev, dtype=torch.float32 if residual else torch.bfloat16)
+    am = name == "lm_head"  # the product's lm_head: greedy-argmax partials, no logits
+    out = (torch.empty(M, N // 128, device=dev, dtype=torch.int64) if am else
+           torch.empty(M, N, device=dev, dtype=torch.float32 if residual else torch.bfloat16))
     res = torch.randn(M, N, device=dev) if residual else None
     gw = ops.GemmWorkspace(dev)
     for i in range(3):
-        ops.gemm(maps[i % copies], xm, M, out, gw, residual=res)
+        ops.gemm(maps[i % copies], xm, M, out, gw, residual=res, argmax=am)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(iters):
-        ops.gemm(maps[i % copies], xm, M, out, gw, residual=res)
+        ops.gemm(maps[i % copies], xm, M, out, gw, residual=res, argmax=am)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / iters
@@ -65,5 +68,5 @@ if __name__ == "__main__":
         _lib.set_knob(k, int(v))
     Ms = [int(a) for a in sys.argv[1:]] or [32, 128, 256, 700, 2048, 4096]
     for M in Ms:
-        for name in SHAPES:
+        for name in (os.environ.get("GEMM_SHAPES") or ",".join(SHAPES)).split(","):
             print(json.dumps(bench(M, name, residual=name in ("o", "down"))), flush=True)
