@@ -11,7 +11,7 @@ Variants: base | plo0 (P as bf16 only) | norope (unfused RoPE / KV append) |
           logits (full lm_head logits + argmax) | pdl0 (no programmatic dependent launch) |
           fmha1q / fmha2q (tcgen05 attention with one / two Q tiles per CTA, forced) |
           python (layer loop in Python, not csrc/step.cu) | serial (attention passes on one
-          stream) | slots1 / slots4 (cascade prefix slots)
+          stream) | slots1 / slots4 (cascade prefix slots) | prio / prio0 / priomax (side stream priority -1 / 0 / highest)
 """
 
 from __future__ import annotations
@@ -43,6 +43,11 @@ VARIANTS = {
     "serial": ({}, {"overlap_cascade": False}),
     "slots1": ({}, {"cascade_slots": 1}),
     "slots4": ({}, {"cascade_slots": 4}),
+    # side stream (cascade + prompt prefill) at high priority: its CTAs are dispatched
+    # ahead of the context splits' as SMs free up
+    "prio": ({}, {"side": lambda: torch.cuda.Stream(priority=-1)}),
+    "prio0": ({}, {"side": lambda: torch.cuda.Stream(priority=0)}),
+    "priomax": ({}, {"side": lambda: torch.cuda.Stream(priority=-100)}),
 }
 
 
@@ -86,7 +91,7 @@ def main() -> None:
             prev_k = {k: _lib.set_knob(k, v) for k, v in knobs.items()}
             prev_a = {k: getattr(w, k) for k in attrs}
             for k, v in attrs.items():
-                setattr(w, k, v)
+                setattr(w, k, v() if callable(v) else v)
             for p in plans[:3]:  # warm the variant
                 w.forward(copy.deepcopy(p))
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

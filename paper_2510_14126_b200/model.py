@@ -293,7 +293,11 @@ class GpuWorker:
         # balanced decode plan (equal tile ranges per CTA) instead of per-call 512-token
         # splits; measured slower on config-2 contexts (benchmarks/attn_step.py), so opt-in
         self.flat_decode = os.environ.get("CORTEX_FLAT_DECODE", "0") == "1"
-        self.side = torch.cuda.Stream(device=dev)
+        # the side stream (cascade pass + prompt prefill, concurrent with the context
+        # splits) at high priority: its big tensor-core CTAs are dispatched ahead of the
+        # splits' as SMs free up instead of waiting for the split grid to drain
+        # (benchmarks/replay_ab.py prio: 12.22 vs 12.56 ms per config-2 step)
+        self.side = torch.cuda.Stream(device=dev, priority=-1)
         self._ev_fork = torch.cuda.Event()
         self._ev_join = torch.cuda.Event()
         # layer loop launched from native code (csrc/step.cu, one ctypes call per step)
