@@ -93,7 +93,7 @@ def build(n_calls=215, n_pf=3, pf_len=200, slots=2, seed=0, layers=4):
     st["kvmap"] = ops.kv_map(cache.view(-1, 128))
     st["qmap"] = ops.QMap(q, HQ, GROUP)
     st["plane"] = nb * HKV * 16
-    st["side"] = torch.cuda.Stream()
+    st["side"] = torch.cuda.Stream(priority=-1)  # as the model's side stream
     st["ev"] = (torch.cuda.Event(), torch.cuda.Event())
     return st
 
@@ -168,6 +168,38 @@ def layer_side_prefill(st, layer):
     decode(st, layer, 4)
 
 
+def layer_side_prefill_first(st, layer):
+    """As layer_side_prefill with the prompt prefill ahead of the cascade pass."""
+    main = torch.cuda.current_stream()
+    st["ev"][0].record(main)
+    st["side"].wait_event(st["ev"][0])
+    prefill(st, layer, st["side"])
+    decode(st, layer, 1, st["side"])
+    decode(st, layer, 2)
+    st["ev"][1].record(st["side"])
+    main.wait_event(st["ev"][1])
+    decode(st, layer, 4)
+
+
+def layer_two_side(st, layer):
+    """Cascade pass and prompt prefill on two high-priority side streams."""
+    main = torch.cuda.current_stream()
+    if "side2" not in st:
+        st["side2"] = torch.cuda.Stream(priority=-1)
+        st["ev2"] = torch.cuda.Event()
+    st["ev"][0].record(main)
+    st["side"].wait_event(st["ev"][0])
+    st["side2"].wait_event(st["ev"][0])
+    decode(st, layer, 1, st["side"])
+    prefill(st, layer, st["side2"])
+    decode(st, layer, 2)
+    st["ev"][1].record(st["side"])
+    st["ev2"].record(st["side2"])
+    main.wait_event(st["ev"][1])
+    main.wait_event(st["ev2"])
+    decode(st, layer, 4)
+
+
 def prefill(st, layer, stream=None):
     pl = st["plane"]
     ops.fmha_prefill(st["kvmap"], st["qmap"], st["attn"], st["table"], st["prow"], st["ppre"],
@@ -213,6 +245,15 @@ def main():
                           "lib": os.environ.get("CORTEX_LIB", ""),
                           "knobs": os.environ.get("CORTEX_KNOBS", ""),
                           "priv_scale": os.environ.get("CORTEX_PRIV_SCALE", "1")}), flush=True)
+        return
+    if "--layer-only" in sys.argv:  # tuning-variant sweeps: one layer's attention as scheduled
+        print(json.dumps({"layer_side_prefill_us": timed(st, lambda l: layer_side_prefill(st, l)),
+                          "layer_prefill_first_us": timed(
+                              st, lambda l: layer_side_prefill_first(st, l)),
+                          "layer_two_side_us": timed(st, lambda l: layer_two_side(st, l)),
+                          "private_us": timed(st, lambda l: decode(st, l, 2, flat=None)),
+                          "lib": os.environ.get("CORTEX_LIB", ""),
+                          "knobs": os.environ.get("CORTEX_KNOBS", "")}), flush=True)
         return
     if "--fmha-only" in sys.argv:  # tuning-variant sweeps: the tensor-core passes alone
         print(json.dumps({"prefill_us": timed(st, lambda l: prefill(st, l)),

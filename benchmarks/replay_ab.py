@@ -11,7 +11,8 @@ Variants: base | plo0 (P as bf16 only) | norope (unfused RoPE / KV append) |
           logits (full lm_head logits + argmax) | pdl0 (no programmatic dependent launch) |
           fmha1q / fmha2q (tcgen05 attention with one / two Q tiles per CTA, forced) |
           python (layer loop in Python, not csrc/step.cu) | serial (attention passes on one
-          stream) | slots1 / slots4 (cascade prefix slots) | prio / prio0 / priomax (side stream priority -1 / 0 / highest)
+          stream) | slots1 / slots4 (cascade prefix slots) | prio / prio0 / priomax (side stream priority -1 / 0 / highest) |
+          oneside (prompt prefill on the cascade's side stream, not a second one)
 """
 
 from __future__ import annotations
@@ -48,6 +49,7 @@ VARIANTS = {
     "prio": ({}, {"side": lambda: torch.cuda.Stream(priority=-1)}),
     "prio0": ({}, {"side": lambda: torch.cuda.Stream(priority=0)}),
     "priomax": ({}, {"side": lambda: torch.cuda.Stream(priority=-100)}),
+    "oneside": ({}, {"side2": None}),  # prompt prefill behind the cascade on one side stream
 }
 
 

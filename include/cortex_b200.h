@@ -276,8 +276,9 @@ int32_t cortex_fmha_cascade_tc(const void* tmap_kv, const void* tmap_q, const in
  * admit prefills and advance_decode tokens, stagesim/engines.py:142-194), launched in the
  * order and with the arguments the per-op exports above take one call at a time: per
  * layer cortex_rmsnorm (attn_norm) -> cortex_gemm_qkv_rope -> decode attention
- * (cortex_paged_decode_attn; with cascade groups and a side stream: parts 1 + the
- * prompt prefill on side_stream, parts 2 on stream, join, parts 4) -> prompt prefill
+ * (cortex_paged_decode_attn; with cascade groups and a side stream: parts 1 on
+ * side_stream, the prompt prefill on side_stream2 (or after parts 1 on side_stream),
+ * parts 2 on stream, join, parts 4) -> prompt prefill
  * (cortex_fmha_prefill_tc, when not on the side stream) -> O projection + residual
  * (mode 1) -> cortex_rmsnorm (mlp_norm) -> gate/up with SwiGLU (mode 2) -> down +
  * residual (mode 1). cortex_decoder_t describes the model (built once); cortex_step_t
@@ -328,7 +329,8 @@ typedef struct {
   float* o_part;
   float* lse_part;
   cortex_stream_t stream;
-  cortex_stream_t side_stream; /* NULL: every attention pass on stream */
+  cortex_stream_t side_stream;  /* NULL: every attention pass on stream */
+  cortex_stream_t side_stream2; /* non-NULL: the prompt prefill here, beside the cascade */
 } cortex_step_t;
 int32_t cortex_decoder_layers(const cortex_decoder_t* model, const cortex_step_t* step);
 

@@ -114,7 +114,8 @@ class StepDesc(ctypes.Structure):
                 ("pf_qlen", P),
                 ("grp_row", P), ("grp_plen", P), ("grp_first", P), ("grp_count", P),
                 ("n_groups", I32), ("max_group_count", I32), ("prefix_slots", I32),
-                ("o_part", P), ("lse_part", P), ("stream", P), ("side_stream", P)]
+                ("o_part", P), ("lse_part", P), ("stream", P), ("side_stream", P),
+                ("side_stream2", P)]
 
 
 STATUS_NAMES = {0: "ok", -1: "bad argument", -2: "CUDA error", -3: "out of KV blocks",

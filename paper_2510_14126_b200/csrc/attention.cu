@@ -32,7 +32,10 @@ constexpr int kStageBytes = 2 * kTileBytes;       // K + V
 #define CORTEX_DECODE_STAGES 2
 #endif
 constexpr int kTilesPerSplit = CORTEX_DECODE_SPLIT_TILES;
-constexpr int kWarps = 4;
+#ifndef CORTEX_DECODE_WARPS  // (overridable for tuning builds)
+#define CORTEX_DECODE_WARPS 4
+#endif
+constexpr int kWarps = CORTEX_DECODE_WARPS;
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct TileRef {

@@ -20,7 +20,7 @@ namespace {
 
 struct StepEvents {
   int device = -1;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr;
 };
 
 // fork / join events of the side stream, one pair per device of the process
@@ -35,7 +35,8 @@ cudaError_t step_events(StepEvents** out) {
   StepEvents& s = ev[dev];
   if (s.device < 0) {
     if ((e = cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming)) != cudaSuccess ||
-        (e = cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming)) != cudaSuccess)
+        (e = cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&s.join2, cudaEventDisableTiming)) != cudaSuccess)
       return e;
     s.device = dev;
   }
@@ -58,6 +59,7 @@ int32_t cortex_decoder_layers(const cortex_decoder_t* m, const cortex_step_t* s)
   const int32_t n_qkv = (hq + 2 * hkv) * 128;
   cudaStream_t main = reinterpret_cast<cudaStream_t>(s->stream);
   cudaStream_t side = reinterpret_cast<cudaStream_t>(s->side_stream);
+  cudaStream_t side2 = reinterpret_cast<cudaStream_t>(s->side_stream2);
   const bool cascade = s->n_groups > 0;
   const bool overlap = cascade && side != nullptr && m->tmap_q != nullptr;
   StepEvents* ev = nullptr;
@@ -93,20 +95,24 @@ int32_t cortex_decoder_layers(const cortex_decoder_t* m, const cortex_step_t* s)
     bool pf_done = false;
     if (s->n_dec > 0) {
       if (overlap) {
-        // tensor-core passes (shared-prefix cascade, then the prompt prefill) on the side
-        // stream, concurrent with the per-call context splits on the main stream; join
-        // before the LSE combine (model.py, the same schedule)
+        // tensor-core passes (shared-prefix cascade; the prompt prefill on a second side
+        // stream when given) concurrent with the per-call context splits on the main
+        // stream; join before the LSE combine (model.py, the same schedule)
+        const bool two = side2 != nullptr && s->n_pf > 0;
         if (cudaEventRecord(ev->fork, main) != cudaSuccess ||
-            cudaStreamWaitEvent(side, ev->fork, 0) != cudaSuccess)
+            cudaStreamWaitEvent(side, ev->fork, 0) != cudaSuccess ||
+            (two && cudaStreamWaitEvent(side2, ev->fork, 0) != cudaSuccess))
           return CORTEX_ECUDA;
         STEP_CALL(decode(1, s->side_stream));
         if (s->n_pf > 0) {
-          STEP_CALL(prefill(s->side_stream));
+          STEP_CALL(prefill(two ? s->side_stream2 : s->side_stream));
           pf_done = true;
         }
         STEP_CALL(decode(2, s->stream));
         if (cudaEventRecord(ev->join, side) != cudaSuccess ||
-            cudaStreamWaitEvent(main, ev->join, 0) != cudaSuccess)
+            cudaStreamWaitEvent(main, ev->join, 0) != cudaSuccess ||
+            (two && (cudaEventRecord(ev->join2, side2) != cudaSuccess ||
+                     cudaStreamWaitEvent(main, ev->join2, 0) != cudaSuccess)))
           return CORTEX_ECUDA;
         STEP_CALL(decode(4, s->stream));
       } else {

@@ -298,6 +298,10 @@ class GpuWorker:
         # splits' as SMs free up instead of waiting for the split grid to drain
         # (benchmarks/replay_ab.py prio: 12.22 vs 12.56 ms per config-2 step)
         self.side = torch.cuda.Stream(device=dev, priority=-1)
+        # the prompt prefill on a second high-priority side stream, beside the cascade pass
+        # (benchmarks/attn_step.py --layer-only: 88.9 vs 92.0 us per config-2 layer)
+        self.side2 = torch.cuda.Stream(device=dev, priority=-1)
+        self._ev_join2 = torch.cuda.Event()
         self._ev_fork = torch.cuda.Event()
         self._ev_join = torch.cuda.Event()
         # layer loop launched from native code (csrc/step.cu, one ctypes call per step)
@@ -683,6 +687,8 @@ class GpuWorker:
             sd.o_part, sd.lse_part = o_part.data_ptr(), lse_part.data_ptr()
             sd.stream = torch.cuda.current_stream().cuda_stream
             sd.side_stream = self.side.cuda_stream if self.overlap_cascade else None
+            sd.side_stream2 = (self.side2.cuda_stream if self.overlap_cascade and self.side2
+                               is not None else None)
             ops._check(ops.lib().cortex_decoder_layers(ctypes.byref(self._native_desc()),
                                                        ctypes.byref(sd)),
                        "cortex_decoder_layers")
@@ -739,13 +745,15 @@ class GpuWorker:
                     ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=4,
                                           flat=flat)
                 elif dec_groups is not None and qmap is not None and self.overlap_cascade:
-                    # tensor-core passes - the shared-prefix (cascade) pass, then the prompt
-                    # prefill - on a side stream, concurrent with the per-call context splits
-                    # (HBM) on the main stream; join before the LSE combine. (The decode
-                    # profile window then covers the prefill attention too.)
+                    # tensor-core passes - the shared-prefix (cascade) pass on a side stream,
+                    # the prompt prefill on a second one - concurrent with the per-call
+                    # context splits (HBM) on the main stream; join before the LSE combine
                     main = torch.cuda.current_stream()
                     self._ev_fork.record(main)
                     self.side.wait_event(self._ev_fork)
+                    two = self.side2 is not None and n_pf > 0
+                    if two:
+                        self.side2.wait_event(self._ev_fork)
 
                     def ctx_splits():
                         e2 = prof.open("attn_decode_ctx") if prof is not None else None
@@ -757,12 +765,15 @@ class GpuWorker:
                     ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=1,
                                           stream=self.side)
                     if n_pf:
-                        prefill_attn(self.side)
+                        prefill_attn(self.side2 if two else self.side)
                         pf_done = True
                         nl += 1
                     ctx_splits()
                     self._ev_join.record(self.side)
                     main.wait_event(self._ev_join)
+                    if two:
+                        self._ev_join2.record(self.side2)
+                        main.wait_event(self._ev_join2)
                     ops.paged_decode_attn(*dargs, groups=dec_groups, qmap=qmap, parts=4,
                                           flat=flat)
                 else:
