@@ -246,7 +246,7 @@ bool knob_ok(int knob, int v) {
 
 extern "C" {
 
-int32_t cortex_abi_version(void) { return 102; }
+int32_t cortex_abi_version(void) { return 103; }
 
 int32_t cortex_dev_set_knob(int32_t knob, int32_t value) {
   if (!knob_ok(knob, value)) return CORTEX_EBADARG;

@@ -43,7 +43,7 @@ def test_library_loads_and_exports_everything():
     lib = _lib.load()
     for name in header_symbols() + header_symbols(DEV_HEADER):
         assert hasattr(lib, name), name
-    assert lib.cortex_abi_version() == 102
+    assert lib.cortex_abi_version() == 103
     # pure host helpers are callable without a GPU
     assert lib.cortex_gemm_splits(32, 6144, 4096) >= 1
     assert lib.cortex_decode_splits(1000, 1300) == 3  # 82 tiles in 32-tile splits
