@@ -62,15 +62,22 @@ CORTEX_DEVICE float block_sum(float v, float* red) {
 __global__ void rmsnorm_kernel(const float* __restrict__ x, const int* __restrict__ rows,
                                const __nv_bfloat16* __restrict__ w, int d, float eps,
                                __nv_bfloat16* __restrict__ y) {
+  // the (immutable) norm weights load before the PDL wait, under the predecessor's tail
+  const bf16x8* wr = reinterpret_cast<const bf16x8*>(w);
+  const int nvec = d / 8;
+  bf16x8 wv[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = threadIdx.x + k * blockDim.x;
+    if (i < nvec) wv[k] = wr[i];
+  }
   pdl_wait();
   pdl_trigger();
   __shared__ float red[32];
   const int r = blockIdx.x;
   const int src = rows ? rows[r] : r;
   const float4* xr = reinterpret_cast<const float4*>(x + static_cast<int64_t>(src) * d);
-  const bf16x8* wr = reinterpret_cast<const bf16x8*>(w);
   bf16x8* yr = reinterpret_cast<bf16x8*>(y + static_cast<int64_t>(r) * d);
-  const int nvec = d / 8;
   // d <= 8 * 4 * blockDim: keep up to 4 vectors per thread in registers
   float f[4][8];
   float ss = 0.f;
@@ -92,7 +99,7 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, const int* __restric
     const int i = threadIdx.x + k * blockDim.x;
     if (i < nvec) {
       float wf[8], o[8];
-      unpack8(wr[i], wf);
+      unpack8(wv[k], wf);
 #pragma unroll
       for (int e = 0; e < 8; ++e) o[e] = f[k][e] * rstd * wf[e];
       yr[i] = pack8(o);
