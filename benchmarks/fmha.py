@@ -115,7 +115,7 @@ if __name__ == "__main__":
                   prefill(0, [8192]), cascade(1000, 115), cascade(8192, 128)):
             r["q_tiles_per_cta"] = {1: 2, 0: 1, -1: "auto"}[q2]
             print(json.dumps(r), flush=True)
-    ops.fmha_set_2q(-1)
+    ops.fmha_set_2q(1)
     if "--slots" in sys.argv:  # the bench's cascade shapes: prefix slots x kernel
         for prefix, n in ((1000, 108), (8192, 128)):
             for sl in (1, 2, 3, 4, 6, 8):
@@ -124,4 +124,4 @@ if __name__ == "__main__":
                     r = cascade(prefix, n, pslots=sl)
                     r["q_tiles_per_cta"] = 2 if q2 else 1
                     print(json.dumps(r), flush=True)
-        ops.fmha_set_2q(-1)
+        ops.fmha_set_2q(1)

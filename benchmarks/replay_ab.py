@@ -9,7 +9,8 @@ kernels' alone (the KV values replayed are stale, the work is the same).
     python benchmarks/replay_ab.py [--record 60] [--rounds 3] [--variants base,plo0,...]
 Variants: base | plo0 (P as bf16 only) | norope (unfused RoPE / KV append) |
           logits (full lm_head logits + argmax) | pdl0 (no programmatic dependent launch) |
-          fmha1q / fmha2q (tcgen05 attention with one / two Q tiles per CTA, forced) |
+          fmha1q / fmha2q / fmhaauto (tcgen05 attention with one / two Q tiles per CTA, or
+          chosen per launch by wave count) |
           python (layer loop in Python, not csrc/step.cu) | serial (attention passes on one
           stream) | slots1 / slots4 (cascade prefix slots) | prio / prio0 / priomax (side stream priority -1 / 0 / highest) |
           oneside (prompt prefill on the cascade's side stream, not a second one)
@@ -40,6 +41,7 @@ VARIANTS = {
     "pdl0": ({"PDL": 0}, {}),
     "fmha1q": ({"FMHA_2Q": 0}, {}),
     "fmha2q": ({"FMHA_2Q": 1}, {}),
+    "fmhaauto": ({"FMHA_2Q": -1}, {}),
     "python": ({}, {"native_layers": False}),
     "serial": ({}, {"overlap_cascade": False}),
     "slots1": ({}, {"cascade_slots": 1}),

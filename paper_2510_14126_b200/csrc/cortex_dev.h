@@ -28,7 +28,7 @@ enum CortexKnob {
   CORTEX_KNOB_SK_MT,          /* cluster split-K: token tiles (-1 planner, 1..4) */
   CORTEX_KNOB_SK_NW,          /* cluster split-K: weight sub-tiles per pair (-1 auto, 2) */
   CORTEX_KNOB_SK_ISSUE,       /* cluster split-K: TMA issuing threads (1, 2 default, 4) */
-  CORTEX_KNOB_FMHA_2Q,        /* tcgen05 attention: -1 per launch, 0 one Q tile, 1 two */
+  CORTEX_KNOB_FMHA_2Q,        /* tcgen05 attention: 1 two Q tiles (default), 0 one, -1 by waves */
   CORTEX_KNOB_FMHA_PLO,       /* tcgen05 attention: P as bf16 hi + lo (1, default) or hi (0) */
   CORTEX_KNOB_COUNT
 };

@@ -223,7 +223,7 @@ __global__ void popcount_kernel(const uint32_t* bitmap, int nwords, int* out_fre
 int g_cortex_knob[CORTEX_KNOB_COUNT] = {
     /* PDL */ 1, /* GEMM_MODE */ 0, /* GEMM_STREAM_K */ -1, /* GEMM_TN */ -1,
     /* GEMM_L2PF */ 0, /* SK_KS */ -1, /* SK_MT */ -1, /* SK_NW */ -1, /* SK_ISSUE */ 2,
-    /* FMHA_2Q */ -1, /* FMHA_PLO */ 1};
+    /* FMHA_2Q */ 1, /* FMHA_PLO */ 1};
 
 namespace {
 bool knob_ok(int knob, int v) {

@@ -120,8 +120,9 @@ def gemm_set_mode(mode: int) -> int:
 
 
 def fmha_set_2q(on: int) -> int:
-    """-1: per-launch choice (default), 1: two Q tiles per CTA in the tcgen05 attention,
-    0: one (the two-tile kernel needs FMHA_PLO = 0)."""
+    """1: two Q tiles per CTA in the tcgen05 attention (default), 0: one, -1: chosen per
+    launch by wave count (the isolated-kernel optimum; in the step, where these passes
+    share the GPU with the context splits, two tiles measured faster)."""
     return _lib.set_knob("FMHA_2Q", on)
 
 

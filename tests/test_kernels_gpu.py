@@ -395,7 +395,7 @@ def test_cascade_decode_attention(cuda, group, plens, impl):
     k0, v0 = _rows(0, nb, hkv)
     from paper_2510_14126_b200 import _lib
 
-    o.fmha_set_2q(0 if impl == "tc1" else 1)
+    prev_2q = o.fmha_set_2q(0 if impl == "tc1" else 1)
     plo = _lib.set_knob("FMHA_PLO", 0 if impl == "tc-bf16p" else 1)
     try:
         o.paged_decode_attn(o.kv_map(cache.view(-1, 128)), q, table, dev(seq_row), dev(seq_pre),
@@ -403,7 +403,7 @@ def test_cascade_decode_attention(cuda, group, plens, impl):
                             lse_part, max_splits, out, groups=groups,
                             qmap=o.QMap(q, hq, group) if impl != "mma" else None, flat=plan)
     finally:
-        o.fmha_set_2q(-1)
+        o.fmha_set_2q(prev_2q)
         _lib.set_knob("FMHA_PLO", plo)
     torch.cuda.synchronize()
     for b in range(B):
@@ -444,12 +444,12 @@ def test_paged_prefill_attention(cuda, group, impl):
     else:
         from paper_2510_14126_b200 import _lib
 
-        o.fmha_set_2q(0 if impl == "tc1" else 1)
+        prev_2q = o.fmha_set_2q(0 if impl == "tc1" else 1)
         plo = _lib.set_knob("FMHA_PLO", 0 if impl == "tc-bf16p" else 1)
         try:
             o.fmha_prefill(kvmap, o.QMap(q, hq, group), out, *args)
         finally:
-            o.fmha_set_2q(-1)
+            o.fmha_set_2q(prev_2q)
             _lib.set_knob("FMHA_PLO", plo)
     torch.cuda.synchronize()
     for b, (prefix, kvlen) in enumerate(specs):
