@@ -443,10 +443,11 @@ def run_arm(args, arm, worker, cfg, desc, barrier, all_reduce, device, local, n_
     ncu_window = timed and os.environ.get("CORTEX_NCU_TIMED") == "1"
     if rt is not None and timed:
         # the dominant kernel class timed with CUDA events inside the timed steps (every
-        # 8th step instrumented: ~0.7 % event overhead); under the ncu capture every step,
+        # 8th step instrumented, every 4th in runs under 100 steps so a 20-step window
+        # still samples 5 step mixes); under the ncu capture every step,
         # so the algorithmic bytes of exactly the captured launches are known
         worker.prof = KernelProfile([dominant, "attn_decode_ctx"] if ncu_window else [dominant],
-                                    every=1 if ncu_window else 8)
+                                    every=1 if ncu_window else (4 if steps < 100 else 8))
     clocks = ClockSampler(local)
     barrier()
     torch.cuda.synchronize()
