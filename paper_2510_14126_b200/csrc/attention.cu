@@ -1186,7 +1186,9 @@ int32_t cortex_paged_decode_attn(
   a.max_splits = max_splits;
   a.cascade = cascade;
   a.slot_off = cascade ? prefix_slots : 0;
-  const int smem = kWarps * kDecodeStages * kStageBytes + 1024 + 256;
+  // stage buffers + their barriers + the 1 KiB alignment slack: 64.06 KiB, so a split CTA
+  // fits beside a 160 KiB tcgen05 attention CTA on one SM
+  const int smem = kWarps * kDecodeStages * (kStageBytes + 8) + 1024;
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(paged_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

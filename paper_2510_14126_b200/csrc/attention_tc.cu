@@ -611,10 +611,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 //   per unit (no cross-warp max exchange), lazy O rescale, P -> TMEM.
 // TMEM: S_A [0,128)  S_B [128,256)  O_A [256,384)  O_B [384,512) (S single-buffered per
 // tile: S_X(t+1) is issued after PV_X(t), which consumed P_X(t) in place, in MMA order).
-// Smem: Q_A 32 KiB, Q_B 32 KiB, 2 K/V stages of 64 KiB, barriers.
+// Smem: Q_A 32 KiB, Q_B 32 KiB, a K ring and a V ring of 32 KiB stages, barriers.
+// K and V have their own rings (K lo | K hi, V lo | V hi per stage, 32 KiB each).
+#ifndef CORTEX_FMHA2_VSTAGES  // (tuning builds: 1 V stage = 160 KiB, a split CTA fits beside)
+#define CORTEX_FMHA2_VSTAGES 2
+#endif
+constexpr int kKStages2 = kStagesTC;
+constexpr int kVStages2 = CORTEX_FMHA2_VSTAGES;
 constexpr int kOffQ2 = 0;
-constexpr int kOffKV2 = 2 * kQBytes;
-constexpr int kOffBar2 = kOffKV2 + kStagesTC * kKVStage;
+constexpr int kOffK2 = 2 * kQBytes;
+constexpr int kOffV2 = kOffK2 + kKStages2 * 2 * kKVHalf;
+constexpr int kOffBar2 = kOffV2 + kVStages2 * 2 * kKVHalf;
 constexpr int kSmemTC2 = kOffBar2 + 256 + 1024;
 
 __global__ void __launch_bounds__(kThreadsTC, 1)
@@ -686,9 +693,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     tma_prefetch_desc(&tmap_q);
     tma_prefetch_desc(&tmap_kv);
     mbar_init(q_full, 1);
-    for (int s = 0; s < kStagesTC; ++s) {
+    for (int s = 0; s < kKStages2; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < kVStages2; ++s) {
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
     }
@@ -718,9 +727,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         tma_load_3d(qd + kQBytes / 2, &tmap_q, q_full, 64, kvh * group, tok0 + x * tpb);
       }
       for (int kt = 0; kt < n_kt; ++kt) {
-        const int s = kt % kStagesTC;
-        const uint32_t ph = (kt / kStagesTC) & 1;
-        uint8_t* st = smem + kOffKV2 + s * kKVStage;
+        const int sk = kt % kKStages2, sv = kt % kVStages2;
+        const uint32_t phk = (kt / kKStages2) & 1, phv = (kt / kVStages2) & 1;
+        uint8_t* stk = smem + kOffK2 + sk * 2 * kKVHalf;
+        uint8_t* stv = smem + kOffV2 + sv * 2 * kKVHalf;
         int rows[kBlocksPerTile];
 #pragma unroll
         for (int j = 0; j < kBlocksPerTile; ++j) {
@@ -728,21 +738,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                                        blk_begin + kt * kBlocksPerTile + j, blk_end);
           rows[j] = static_cast<int>((static_cast<int64_t>(b.block) * a.n_kv_heads + kvh) * kBlk);
         }
-        mbar_wait_guard(&k_empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&k_full[s], 2 * kKVHalf);
+        mbar_wait_guard(&k_empty[sk], phk ^ 1);
+        mbar_arrive_expect_tx(&k_full[sk], 2 * kKVHalf);
 #pragma unroll
         for (int j = 0; j < kBlocksPerTile; ++j) {
           const int off = j * kBlk * 128;
-          tma_load_2d(st + 0 * kKVHalf + off, &tmap_kv, &k_full[s], 0, static_cast<int>(a.k_row0) + rows[j]);
-          tma_load_2d(st + 1 * kKVHalf + off, &tmap_kv, &k_full[s], 64, static_cast<int>(a.k_row0) + rows[j]);
+          tma_load_2d(stk + 0 * kKVHalf + off, &tmap_kv, &k_full[sk], 0, static_cast<int>(a.k_row0) + rows[j]);
+          tma_load_2d(stk + 1 * kKVHalf + off, &tmap_kv, &k_full[sk], 64, static_cast<int>(a.k_row0) + rows[j]);
         }
-        mbar_wait_guard(&v_empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&v_full[s], 2 * kKVHalf);
+        mbar_wait_guard(&v_empty[sv], phv ^ 1);
+        mbar_arrive_expect_tx(&v_full[sv], 2 * kKVHalf);
 #pragma unroll
         for (int j = 0; j < kBlocksPerTile; ++j) {
           const int off = j * kBlk * 128;
-          tma_load_2d(st + 2 * kKVHalf + off, &tmap_kv, &v_full[s], 0, static_cast<int>(a.v_row0) + rows[j]);
-          tma_load_2d(st + 3 * kKVHalf + off, &tmap_kv, &v_full[s], 64, static_cast<int>(a.v_row0) + rows[j]);
+          tma_load_2d(stv + 0 * kKVHalf + off, &tmap_kv, &v_full[sv], 0, static_cast<int>(a.v_row0) + rows[j]);
+          tma_load_2d(stv + 1 * kKVHalf + off, &tmap_kv, &v_full[sv], 64, static_cast<int>(a.v_row0) + rows[j]);
         }
       }
     }
@@ -755,9 +765,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       const int nx = has_b ? 2 : 1;
       mbar_wait_guard(q_full, 0);
       auto issue_s = [&](int kt, int x, int h) {  // S_x(kt, h) -> TMEM S_x cols [64h, +64)
-        const int s = kt % kStagesTC;
+        const int s = kt % kKStages2;
         const uint32_t q_addr = smem_u32(smem + kOffQ2 + x * kQBytes);
-        const uint32_t k_addr = smem_u32(smem + kOffKV2 + s * kKVStage) + h * 64 * 128;
+        const uint32_t k_addr = smem_u32(smem + kOffK2 + s * 2 * kKVHalf) + h * 64 * 128;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t off = (kk >> 2) * kKVHalf + (kk & 3) * 32;
@@ -769,8 +779,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         umma_commit(&s_full[2 * x + h]);
       };
       auto issue_pv = [&](int kt, int x, int h) {  // O_x += P_x(kt, h) V(kt, keys of h)
-        const int s = kt % kStagesTC;
-        const uint32_t v_addr = smem_u32(smem + kOffKV2 + s * kKVStage + 2 * kKVHalf);
+        const int s = kt % kVStages2;
+        const uint32_t v_addr = smem_u32(smem + kOffV2 + s * 2 * kKVHalf);
         const uint32_t p_tmem = tmem + 128 * x + 64 * h;
         const uint32_t o_tmem = tmem + 256 + 128 * x;
         // P = hi + lo (p_lo): hi in this half's first 32 columns, lo in the next 32
@@ -795,10 +805,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         umma_commit(&k_empty[0]);
       }
       for (int kt = 0; kt < n_kt; ++kt) {
-        const int s = kt % kStagesTC;
+        const int s = kt % kVStages2;
         const bool more = kt + 1 < n_kt;
-        const int s1 = (kt + 1) % kStagesTC;
-        mbar_wait_guard(&v_full[s], (kt / kStagesTC) & 1);
+        const int s1 = (kt + 1) % kKStages2;
+        mbar_wait_guard(&v_full[s], (kt / kVStages2) & 1);
         for (int h = 0; h < 2; ++h) {
           for (int x = 0; x < nx; ++x) {
             mbar_wait_guard(&p_full[2 * x + h], kt & 1);
@@ -806,7 +816,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             issue_pv(kt, x, h);
             if (more) {  // S_x(kt+1, h) into the half PV_x(kt, h) just released
               if (h == 0 && x == 0) {
-                mbar_wait_guard(&k_full[s1], ((kt + 1) / kStagesTC) & 1);
+                mbar_wait_guard(&k_full[s1], ((kt + 1) / kKStages2) & 1);
                 tc_fence_after();
               }
               issue_s(kt + 1, x, h);
