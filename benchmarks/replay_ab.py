@@ -51,7 +51,8 @@ VARIANTS = {
     "prio": ({}, {"side": lambda: torch.cuda.Stream(priority=-1)}),
     "prio0": ({}, {"side": lambda: torch.cuda.Stream(priority=0)}),
     "priomax": ({}, {"side": lambda: torch.cuda.Stream(priority=-100)}),
-    "oneside": ({}, {"side2": None}),  # prompt prefill behind the cascade on one side stream
+    "oneside": ({}, {"side2": None}),
+    "cascade_lo": ({}, {"side": lambda: torch.cuda.Stream(priority=0)}),  # prefill high only  # prompt prefill behind the cascade on one side stream
 }
 
 
