@@ -41,12 +41,14 @@ def _plans(rng):
     return plans
 
 
-def _run(cuda, native: bool, overlap: bool):
+def _run(cuda, native: bool, overlap: bool, two_side: bool = True):
     torch.manual_seed(0)
     w = GpuWorker(CFG, cuda, n_blocks=64, n_rows=8, row_cols=32, max_tokens=512, max_out=16,
                   hist_cols=16, max_seq_tokens=512, seed=3)
     w.native_layers = native
     w.overlap_cascade = overlap
+    if not two_side:
+        w.side2 = None
     npb = (P + 15) // 16
     tab = torch.zeros(8, 32, dtype=torch.int32)
     tab[0, :npb] = torch.arange(npb)
@@ -78,3 +80,15 @@ def test_native_layers_bit_identical(cuda, overlap):
             assert torch.equal(a, b), (i, name)
     assert torch.equal(cache_n, cache_p)
     assert torch.isfinite(got[-1][0]).all()
+
+
+def test_stream_schedules_bit_identical(cuda):
+    """The attention passes' stream placement (two side streams, one, or all on the main
+    stream) changes only the overlap, never a value."""
+    ref, cache_ref, _ = _run(cuda, True, True)
+    for overlap, two in ((True, False), (False, True)):
+        got, cache, _ = _run(cuda, True, overlap, two)
+        for i, (g, w) in enumerate(zip(got, ref)):
+            for name, a, b in zip(("x", "q", "attn", "out_tok", "slot_tok"), g, w):
+                assert torch.equal(a, b), (overlap, two, i, name)
+        assert torch.equal(cache, cache_ref)
