@@ -200,6 +200,25 @@ def layer_two_side(st, layer):
     decode(st, layer, 4)
 
 
+def layer_two_side_pf_first(st, layer):
+    """layer_two_side with the prompt prefill launched ahead of the cascade pass."""
+    main = torch.cuda.current_stream()
+    if "side2" not in st:
+        st["side2"] = torch.cuda.Stream(priority=-1)
+        st["ev2"] = torch.cuda.Event()
+    st["ev"][0].record(main)
+    st["side"].wait_event(st["ev"][0])
+    st["side2"].wait_event(st["ev"][0])
+    prefill(st, layer, st["side2"])
+    decode(st, layer, 1, st["side"])
+    decode(st, layer, 2)
+    st["ev"][1].record(st["side"])
+    st["ev2"].record(st["side2"])
+    main.wait_event(st["ev"][1])
+    main.wait_event(st["ev2"])
+    decode(st, layer, 4)
+
+
 def prefill(st, layer, stream=None):
     pl = st["plane"]
     ops.fmha_prefill(st["kvmap"], st["qmap"], st["attn"], st["table"], st["prow"], st["ppre"],
@@ -251,6 +270,8 @@ def main():
                           "layer_prefill_first_us": timed(
                               st, lambda l: layer_side_prefill_first(st, l)),
                           "layer_two_side_us": timed(st, lambda l: layer_two_side(st, l)),
+                          "layer_two_side_pf_first_us": timed(
+                              st, lambda l: layer_two_side_pf_first(st, l)),
                           "private_us": timed(st, lambda l: decode(st, l, 2, flat=None)),
                           "lib": os.environ.get("CORTEX_LIB", ""),
                           "knobs": os.environ.get("CORTEX_KNOBS", "")}), flush=True)

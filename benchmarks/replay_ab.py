@@ -52,7 +52,9 @@ VARIANTS = {
     "prio0": ({}, {"side": lambda: torch.cuda.Stream(priority=0)}),
     "priomax": ({}, {"side": lambda: torch.cuda.Stream(priority=-100)}),
     "oneside": ({}, {"side2": None}),
-    "cascade_lo": ({}, {"side": lambda: torch.cuda.Stream(priority=0)}),  # prefill high only  # prompt prefill behind the cascade on one side stream
+    "cascade_lo": ({}, {"side": lambda: torch.cuda.Stream(priority=0)}),  # prefill high only
+    "casc_top": ({}, {"side": lambda: torch.cuda.Stream(priority=-3)}),  # cascade above prefill
+    "pf_top": ({}, {"side2": lambda: torch.cuda.Stream(priority=-3)}),   # prefill above cascade  # prompt prefill behind the cascade on one side stream
 }
 
 
