@@ -606,7 +606,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 // softmax runs. The work unit is half a key tile (64 keys): S of one half is computed
 // while the same warpgroup's softmax works on the other half (S_X(t+1, h) is issued
 // right behind PV_X(t, h), which frees those TMEM columns):
-//   MMA warp: S(0,0) S(0,1) | per half h: PV_A(t,h) S_A(t+1,h) PV_B(t,h) S_B(t+1,h) | ...
+//   MMA warp: S(0,0) S(0,1) | per tile X, half h in order: PV_X(t,h) S_X(t+1,h), the two
+//   tiles' units interleaved in the order their P becomes ready | ...
 //   softmax warpgroup A (warps 2-5) and B (warps 6-9): one thread per query row, 64 keys
 //   per unit (no cross-warp max exchange), lazy O rescale, P -> TMEM.
 // TMEM: S_A [0,128)  S_B [128,256)  O_A [256,384)  O_B [384,512) (S single-buffered per
@@ -809,20 +810,33 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const bool more = kt + 1 < n_kt;
         const int s1 = (kt + 1) % kKStages2;
         mbar_wait_guard(&v_full[s], (kt / kVStages2) & 1);
-        for (int h = 0; h < 2; ++h) {
-          for (int x = 0; x < nx; ++x) {
-            mbar_wait_guard(&p_full[2 * x + h], kt & 1);
-            tc_fence_after();
-            issue_pv(kt, x, h);
-            if (more) {  // S_x(kt+1, h) into the half PV_x(kt, h) just released
-              if (h == 0 && x == 0) {
-                mbar_wait_guard(&k_full[s1], ((kt + 1) / kKStages2) & 1);
-                tc_fence_after();
+        // PV + next S of whichever tile's P is ready first (the order within a tile is
+        // fixed: h = 0 then 1), so a slower softmax warpgroup does not hold the other
+        // tile's MMAs (prefill 41.6 vs 42.5 us, benchmarks/attn_step.py --fmha-only)
+        {
+          int next_h[2] = {0, nx > 1 ? 0 : 2};
+          bool k_ready = !more;
+          const long long t0 = clock64();
+          while (next_h[0] < 2 || next_h[1] < 2) {
+            for (int x = 0; x < 2; ++x) {
+              const int h = next_h[x];
+              if (h >= 2 || !mbar_test_wait(&p_full[2 * x + h], kt & 1)) continue;
+              tc_fence_after();
+              issue_pv(kt, x, h);
+              if (more) {
+                if (!k_ready) {
+                  mbar_wait_guard(&k_full[s1], ((kt + 1) / kKStages2) & 1);
+                  tc_fence_after();
+                  k_ready = true;
+                }
+                issue_s(kt + 1, x, h);
               }
-              issue_s(kt + 1, x, h);
+              next_h[x] = h + 1;
             }
+            if (clock64() - t0 > (8ll << 30)) __trap();
           }
         }
+
         umma_commit(&v_empty[s]);
         if (more) umma_commit(&k_empty[s1]);
       }
