@@ -45,6 +45,7 @@ VARIANTS = {
     "python": ({}, {"native_layers": False}),
     "serial": ({}, {"overlap_cascade": False}),
     "slots1": ({}, {"cascade_slots": 1}),
+    "slots3": ({}, {"cascade_slots": 3}),
     "slots4": ({}, {"cascade_slots": 4}),
     # side stream (cascade + prompt prefill) at high priority: its CTAs are dispatched
     # ahead of the context splits' as SMs free up
