@@ -46,6 +46,13 @@ VARIANTS = {
     "serial": ({}, {"overlap_cascade": False}),
     "slots1": ({}, {"cascade_slots": 1}),
     "slots3": ({}, {"cascade_slots": 3}),
+    "ovh0": ({"GEMM_TILE_OVH": 0}, {}),    # 2-SM tile planner's per-tile overhead (32)
+    "ovh16": ({"GEMM_TILE_OVH": 16}, {}),
+    "ovh64": ({"GEMM_TILE_OVH": 64}, {}),
+    "ovh96": ({"GEMM_TILE_OVH": 96}, {}),
+    "ovh128": ({"GEMM_TILE_OVH": 128}, {}),
+    "ovh192": ({"GEMM_TILE_OVH": 192}, {}),
+    "ovh256": ({"GEMM_TILE_OVH": 256}, {}),
     "slots4": ({}, {"cascade_slots": 4}),
     # side stream (cascade + prompt prefill) at high priority: its CTAs are dispatched
     # ahead of the context splits' as SMs free up

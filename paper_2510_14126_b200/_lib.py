@@ -80,7 +80,7 @@ DEV_SIGNATURES: dict[str, list] = {
 # knob ids (csrc/cortex_dev.h, enum CortexKnob)
 KNOBS = {name: i for i, name in enumerate(
     ["PDL", "GEMM_MODE", "GEMM_STREAM_K", "GEMM_TN", "GEMM_L2PF", "SK_KS", "SK_MT", "SK_NW",
-     "SK_ISSUE", "FMHA_2Q", "FMHA_PLO"])}
+     "SK_ISSUE", "FMHA_2Q", "FMHA_PLO", "GEMM_TILE_OVH"])}
 
 class RopeEpilogue(ctypes.Structure):
     """cortex_rope_epilogue_t (include/cortex_b200.h)."""

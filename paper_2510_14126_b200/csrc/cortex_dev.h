@@ -30,6 +30,7 @@ enum CortexKnob {
   CORTEX_KNOB_SK_ISSUE,       /* cluster split-K: TMA issuing threads (1, 2 default, 4) */
   CORTEX_KNOB_FMHA_2Q,        /* tcgen05 attention: 1 two Q tiles (default), 0 one, -1 by waves */
   CORTEX_KNOB_FMHA_PLO,       /* tcgen05 attention: P as bf16 hi + lo (1, default) or hi (0) */
+  CORTEX_KNOB_GEMM_TILE_OVH,  /* 2-SM tile planner: per-tile overhead in token columns (32) */
   CORTEX_KNOB_COUNT
 };
 

@@ -578,8 +578,9 @@ void cortex_gemm2_plan(int M, int N, int K, int n_sms, int* tn_out, int* sk_out)
     for (int sk = 0; sk <= 1; ++sk) {
       if (force >= 0 && sk != force) continue;
       const long waves = (units + pairs - 1) / pairs;
-      const double cost = sk ? static_cast<double>(units) / pairs * (tn + 32.0) * 1.06 + 16.0
-                             : waves * (tn + 32.0);
+      const double ovh = g_cortex_knob[CORTEX_KNOB_GEMM_TILE_OVH];
+      const double cost = sk ? static_cast<double>(units) / pairs * (tn + ovh) * 1.06 + 16.0
+                             : waves * (tn + ovh);
       if (best < 0 || cost < best - 1e-9) {
         best = cost;
         *tn_out = tn;

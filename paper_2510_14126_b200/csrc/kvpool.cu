@@ -223,7 +223,8 @@ __global__ void popcount_kernel(const uint32_t* bitmap, int nwords, int* out_fre
 int g_cortex_knob[CORTEX_KNOB_COUNT] = {
     /* PDL */ 1, /* GEMM_MODE */ 0, /* GEMM_STREAM_K */ -1, /* GEMM_TN */ -1,
     /* GEMM_L2PF */ 0, /* SK_KS */ -1, /* SK_MT */ -1, /* SK_NW */ -1, /* SK_ISSUE */ 2,
-    /* FMHA_2Q */ 1, /* FMHA_PLO */ 1};
+    /* FMHA_2Q */ 1, /* FMHA_PLO */ 1,
+    /* GEMM_TILE_OVH */ 32};
 
 namespace {
 bool knob_ok(int knob, int v) {
@@ -239,6 +240,7 @@ bool knob_ok(int knob, int v) {
     case CORTEX_KNOB_SK_ISSUE: return v == 1 || v == 2 || v == 4;
     case CORTEX_KNOB_FMHA_2Q: return v >= -1 && v <= 1;
     case CORTEX_KNOB_FMHA_PLO: return v == 0 || v == 1;
+    case CORTEX_KNOB_GEMM_TILE_OVH: return v >= 0 && v <= 256;
     default: return false;
   }
 }
