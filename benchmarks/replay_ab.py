@@ -53,6 +53,10 @@ VARIANTS = {
     "ovh128": ({"GEMM_TILE_OVH": 128}, {}),
     "ovh192": ({"GEMM_TILE_OVH": 192}, {}),
     "ovh256": ({"GEMM_TILE_OVH": 256}, {}),
+    "l2pf8": ({"GEMM_L2PF": 8}, {}),       # weight K blocks prefetched to L2 pre-PDL-wait
+    "l2pf32": ({"GEMM_L2PF": 32}, {}),
+    "skiss1": ({"SK_ISSUE": 1}, {}),       # split-K TMA issuing threads (2)
+    "skiss4": ({"SK_ISSUE": 4}, {}),
     "slots4": ({}, {"cascade_slots": 4}),
     # side stream (cascade + prompt prefill) at high priority: its CTAs are dispatched
     # ahead of the context splits' as SMs free up
