@@ -36,3 +36,19 @@ def test_descriptor_layout_matches_header(tmp_path):
         assert got[(cname, "size")] == ctypes.sizeof(cls), cname
         for f, _ in cls._fields_:
             assert got[(cname, f)] == getattr(cls, f).offset, (cname, f)
+
+
+def test_decoder_layers_rejects_bad_descriptors():
+    """Argument validation happens before any CUDA call (runs without a GPU): a missing
+    descriptor, an empty step, a layer range outside the model, or no tcgen05 Q map."""
+    from paper_2510_14126_b200 import _lib
+
+    lib = _lib.load()
+    m, st = _lib.DecoderDesc(), _lib.StepDesc()
+    assert lib.cortex_decoder_layers(None, ctypes.byref(st)) == -1
+    assert lib.cortex_decoder_layers(ctypes.byref(m), None) == -1
+    m.n_layers, m.hq, m.hkv = 2, 8, 2
+    st.n_tok, st.n_dec, st.layer_begin, st.layer_end = 4, 4, 0, 2
+    assert lib.cortex_decoder_layers(ctypes.byref(m), ctypes.byref(st)) == -1  # no weights
+    st.layer_end = 3
+    assert lib.cortex_decoder_layers(ctypes.byref(m), ctypes.byref(st)) == -1  # past n_layers
